@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Bench for the B200 block-matching library (G-BM3D hot path, arXiv 2103.10765).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c4] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path (grid, per-displacement SSD box
+sums, top-K selection, table write) over the configured synthetic workload.  Default workload:
+c3 (2048^2, P8 s3 r19 K32 -- BASELINE.json configs[3]); c4 (64 x 512^2, K16) is measured
+beside it at N=1 and reported under "also".  Rank 0 prints ONE JSON line.  For N > 1 run
+under torchrun: c3 is row-sharded with halos and the tables gathered to rank 0 over NCCL;
+c4 is batch-split (no collective).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+INT_LANES_PER_SM = 128      # 4 SMSP x 32 lanes issue; IADD3 (alu) + IMAD (fma) pipes, 64 each
+N_SMS = 148
+
+
+def a_eval(stride: int) -> int:
+    """Algorithmic int32 ops per candidate evaluation of the SSD form:
+    per pixel-displacement 1 ISUB + 1 IMUL + 1 IADD3 (vertical running sum), 1/s IADD3
+    (horizontal), 1/s^2 compare -> 3 s^2 + s + 1 per evaluation."""
+    return 3 * stride * stride + stride + 1
+
+
+def total_evals(H, W, P, s, r):
+    def axis(L):
+        pos = list(range(0, L - P + 1, s))
+        if (L - P) % s:
+            pos.append(L - P)
+        return [min(L - P, p + r) - max(0, p - r) + 1 for p in pos]
+    wy, wx = axis(H), axis(W)
+    return sum(a * b - 1 for a in wy for b in wx), len(wy) * len(wx)
+
+
+class ClockSampler:
+    """nvidia-smi sampler of SM clocks and throttle reasons (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        top = max(sm) if sm else 0
+        load = [v for v in sm if v >= 0.5 * top] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows),
+                "power_w_max": max((num(r[2]) or 0.0) for r in self.rows)}
+
+
+def _events_ms(fn, stream, torch):
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    fn()
+    e.record(stream)
+    return s, e
+
+
+def measure_device(step, K, W, flush, torch, dist_barrier=None, soak_s=1.0):
+    """W warm-up steps, a clock soak, then exactly K timed steps (per-step CUDA events on the
+    launching stream; the L2 flush between steps is outside the events)."""
+    stream = torch.cuda.current_stream()
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    t_end = time.time() + soak_s  # clock sampling window before the timed region
+    while time.time() < t_end:
+        step()
+        torch.cuda.synchronize()
+    if dist_barrier:
+        dist_barrier()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(K):
+        flush()
+        evs.append(_events_ms(step, stream, torch))
+    torch.cuda.synchronize()
+    if dist_barrier:
+        dist_barrier()
+    return [s.elapsed_time(e) for s, e in evs]
+
+
+def oracle_sample_rate(cfg, call, target_s, seed=0, threads=0):
+    """Time the oracle (as it stands) on a random sample of the workload's references, sized to
+    ~target_s seconds.  Returns (refs/s, evals/s, n_refs, seconds, threads)."""
+    import numpy as np
+
+    import oracle
+    from synth import make_image
+    img = make_image(cfg.H, cfg.W, cfg.n_rect, cfg.n_tex, cfg.sigma, cfg.seeds[0])
+    gy = oracle.grid(cfg.H, call.patch, call.stride)
+    gx = oracle.grid(cfg.W, call.patch, call.stride)
+    rng = np.random.default_rng(seed)
+
+    def run(n):
+        py = rng.integers(0, len(gy), n)
+        px = rng.integers(0, len(gx), n)
+        t0 = time.perf_counter()
+        oracle.block_match_refs(img, call.patch, call.stride, call.radius, call.K, call.tau, py,
+                                px, threads=threads)
+        return time.perf_counter() - t0
+
+    n0 = 2000
+    t0 = run(n0)
+    n = max(n0, int(n0 * target_s / max(t0, 1e-3)))
+    t = run(n)
+    evals_total, refs_total = total_evals(cfg.H, cfg.W, call.patch, call.stride, call.radius)
+    ev_per_ref = evals_total / refs_total
+    return n / t, n * ev_per_ref / t, n, t, threads or oracle.max_threads()
+
+
+def bench_reference(args, cfg, call, rank):
+    """--impl reference: the oracle as it stands on the host cores; each step one bounded
+    sample of the workload (~3 s)."""
+    if rank != 0:
+        return
+    import oracle
+    threads = oracle.max_threads()
+    rates = []
+    per = None
+    for i in range(args.warmup + args.steps):
+        rate, evr, n, t, thr = oracle_sample_rate(cfg, call, 3.0, seed=i)
+        if i >= args.warmup:
+            rates.append(rate)
+            per = (n, t)
+    value = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": "ref patches matched/sec", "value": value,
+        "unit": "refs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * per[1], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "i64", "data": "synthetic",
+        "config": workload_config(cfg, call, args),
+        "cpu_baseline": {"value": value, "unit": "refs/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{per[0]} random references of {cfg.name} per step"},
+        "e2e": {"value": value, "unit": "refs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, call, args):
+    return {"workload": f"{cfg.name}: {cfg.note}", "H": cfg.H, "W": cfg.W, "B": cfg.B,
+            "patch": call.patch, "stride": call.stride, "radius": call.radius, "K": call.K,
+            "tau": call.tau, "parallelism": ("rows" if cfg.name == "c3" else "batch") +
+            f"x{args.gpus}", "l2": "256 MiB write between timed steps (outside the events)"}
+
+
+def load_traffic(name):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(name)
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
+    """N = 1 measurement of one workload; returns the JSON dict."""
+    from synth import config_images
+    dev = torch.device("cuda", 0)
+    imgs = torch.from_numpy(config_images(cfg)).to(dev)
+    img = imgs if cfg.B > 1 else imgs[0].contiguous()
+    assert g.check_range(img, call.patch), "synthetic image outside the int32 domain"
+    Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
+    shape = ((cfg.B,) if cfg.B > 1 else ()) + (Ry, Rx, call.K)
+    outs = (torch.empty(shape, dtype=torch.int32, device=dev),
+            torch.empty(shape, dtype=torch.int32, device=dev),
+            torch.empty(shape[:-1], dtype=torch.int32, device=dev))
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def step():
+        g.block_match(img, call.patch, call.stride, call.radius, call.K, call.tau, check=False,
+                      method=args.method, out=outs)
+
+    step()
+    launches_per_step = g.last_launch_count()
+    sampler = ClockSampler(0).start()
+    times = measure_device(step, args.steps, args.warmup, flush_buf.zero_, torch)
+    sampler.stop()
+    clocks = sampler.summary()
+    ms = statistics.mean(times)
+    evals1, refs1 = total_evals(cfg.H, cfg.W, call.patch, call.stride, call.radius)
+    evals, refs = evals1 * cfg.B, refs1 * cfg.B
+    value = refs / (ms * 1e-3)
+    A = a_eval(call.stride)
+    achieved = evals * A / (ms * 1e-3) / 1e12
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    peak = INT_LANES_PER_SM * N_SMS * sm_max * 1e6 / 1e12
+    line = {
+        "metric": "ref patches matched/sec", "value": value, "unit": "refs/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "i32", "data": "synthetic",
+        "config": workload_config(cfg, call, args),
+        "gevals_per_s": evals / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TOP/s",
+                     "frac": achieved / peak, "traffic": load_traffic(cfg.name),
+                     "ops_per_eval": A, "evals_per_launch": evals,
+                     "peak_basis": f"{INT_LANES_PER_SM} int32 lanes/clk/SM x {N_SMS} SMs x "
+                                   f"{sm_max:.0f} MHz (B300_MICROARCH pipe rates; DESIGN.md)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "kernel_ms": {"mean": ms, "min": min(times), "max": max(times)},
+    }
+    if want_e2e:
+        line["e2e"] = run_e2e(args, cfg, call, torch, g)
+    if want_cpu:
+        rate, evr, n, t, thr = oracle_sample_rate(cfg, call, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "refs/s", "cores": thr, "kind": "oracle",
+                                "sample": f"{n} random references of {cfg.name} "
+                                          f"({n * evals1 / refs1:.3g} evals) in {t:.1f} s",
+                                "gevals_per_s": evr / 1e9}
+    del imgs, outs, flush_buf
+    return line
+
+
+def run_e2e(args, cfg, call, torch, g):
+    """Same metric through the host-buffer C-ABI entry: pinned H2D of the images, the match,
+    D2H of idx/dist/n_valid, all inside each timed step."""
+    from synth import config_images
+    h = torch.from_numpy(config_images(cfg)).pin_memory()
+    Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
+    B = cfg.B
+    ws = torch.empty(g.host_workspace_bytes(B, cfg.H, cfg.W, call.patch, call.stride, call.K),
+                     dtype=torch.uint8, device="cuda")
+    out = (torch.empty((B, Ry, Rx, call.K), dtype=torch.int32, pin_memory=True),
+           torch.empty((B, Ry, Rx, call.K), dtype=torch.int32, pin_memory=True),
+           torch.empty((B, Ry, Rx), dtype=torch.int32, pin_memory=True))
+
+    def step():
+        g.block_match_host(h, call.patch, call.stride, call.radius, call.K, call.tau,
+                           workspace=ws, out=out)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    _, refs1 = total_evals(cfg.H, cfg.W, call.patch, call.stride, call.radius)
+    return {"value": refs1 * B / t, "unit": "refs/s", "ms_per_step": 1e3 * t,
+            "h2d_bytes_per_step": int(h.numel() * 2),
+            "d2h_bytes_per_step": int(sum(o.numel() * 4 for o in out))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default="auto", choices=["auto", "ssd", "product", "direct"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-also", action="store_true", help="skip the secondary c4 line")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    call = cfg.calls[0]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        bench_reference(args, cfg, call, rank)
+        return
+
+    import torch
+    import paper_2103_10765_b200 as g
+    if world > 1 or args.gpus > 1:
+        from paper_2103_10765_b200 import dist as gdist
+        line = gdist.bench_multi(args, cfg, call)
+        if line is not None and rank == 0:
+            print(json.dumps(line), flush=True)
+        return
+    torch.cuda.set_device(0)
+    line = run_ours_single(args, cfg, call, torch, g)
+    if not args.no_also and args.config != "c4":
+        c4 = CONFIGS["c4"]
+        also = run_ours_single(args, c4, c4.calls[0], torch, g, want_e2e=True, want_cpu=False)
+        line["also"] = {"c4": {k: also[k] for k in ("value", "unit", "ms_per_step",
+                                                    "gevals_per_s", "roofline", "e2e",
+                                                    "config", "clocks")}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

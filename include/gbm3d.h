@@ -1,0 +1,135 @@
+/*
+ * gbm3d.h -- C ABI of the B200 (sm_100a) block-matching library for G-BM3D
+ * (Sanders & Larkin, arXiv 2103.10765).  Library: paper_2103_10765_b200/libgbm3d.so.
+ *
+ * What every entry computes (PAPER.md = /root/reference/PAPER.md, line numbers):
+ *   For each reference patch rho = (ry, rx) on the grid R_y x R_x with
+ *     R = {0, s, 2s, ... <= L-P} U {L-P}                 (tiles at (pN,qN), PAPER.md:154-156;
+ *                                                         DESIGN.md reading R3)
+ *   and each candidate c in the clamped window |c - rho|_inf <= radius, c != rho
+ *                                                        (local search; R2)
+ *     d(rho, c) = ||Z_rho - Z_c||_2^2 = sum_{i,j<P} (Z[ry+i][rx+j] - Z[cy+i][cx+j])^2
+ *                                                        (Eq. (1))
+ *   keep the K-1 smallest keys (d, idx(c)) with d < tau (strict, Eq. (1); R5, R6), after
+ *   the reference itself in slot 0 with d = 0:  this is S^K_pq on the
+ *   local window, "exactly 15 matches" for K = 16 (R4).  Missing slots are
+ *   "padded with the reference block": idx = idx(rho), dist = -1 (R7).
+ *   idx(c) = cy * W + cx (raster index of the candidate's top-left pixel).
+ *   The kernels evaluate d organised by displacement delta = c - rho: the shifted-difference
+ *   image (Z - S_delta Z)^2 box-summed over P x P (Prop. 1 with an all-ones block,
+ *   PAPER.md:89-113), in exact int32 arithmetic -- results are bit-identical to the
+ *   definition above.
+ *
+ * Layouts (all row-major, contiguous):
+ *   image      int16  [H][W]          batched: [B][H][W]
+ *   idx, dist  int32  [Ry][Rx][K]     batched: [B][Ry][Rx][K]
+ *   n_valid    int32  [Ry][Rx]        batched: [B][Ry][Rx]  (nullable)
+ *   references in raster order of the grid; slots hold ranks 0..K-1.
+ *
+ * Ownership: the caller allocates and owns every buffer.  Device entries take DEVICE
+ * pointers and enqueue on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ * stream); they return after enqueueing (results are ready when the stream is).  They hold
+ * no state, allocate nothing, and are reentrant: any number of concurrent calls on distinct
+ * streams is allowed.  Outputs are undefined after any error.
+ *
+ * Precondition (exactness domain, reading R10): P^2 * (max(Z) - min(Z))^2 <=
+ * 2^31 - 1, so every distance fits int32.  gbm3d_check_range verifies it; the device entries
+ * do not (they are the hot path).
+ *
+ * Supported sizes: 1 <= patch <= 16, 0 <= radius <= 32, 1 <= K <= 64, stride >= 1,
+ * H, W >= patch, H*W < 2^31.  Larger patch/radius/K return GBM3D_ERR_UNSUPPORTED.
+ */
+#ifndef GBM3D_H
+#define GBM3D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* tau value meaning "no threshold" (d < INT64_MAX always holds). */
+#define GBM3D_TAU_NONE INT64_MAX
+
+enum {
+    GBM3D_OK = 0,
+    GBM3D_ERR_ARG = -1,         /* null pointer, bad size/parameter; nothing enqueued     */
+    GBM3D_ERR_RANGE = -2,       /* image violates P^2 (max-min)^2 <= 2^31-1               */
+    GBM3D_ERR_UNSUPPORTED = -3, /* patch > 16, radius > 32 or K > 64                      */
+    GBM3D_ERR_CUDA = -4         /* a CUDA launch/copy error (async faults surface at sync) */
+};
+
+/* Matching algorithm selector for gbm3d_block_match_ex. */
+enum {
+    GBM3D_METHOD_AUTO = 0,     /* fastest exact kernel available for the shape            */
+    GBM3D_METHOD_SSD = 1,      /* displacement-organised shifted-difference box sums      */
+    GBM3D_METHOD_PRODUCT = 2,  /* Eq. (2) product form: norms + box sums of Z * S_delta Z */
+    GBM3D_METHOD_DIRECT = 3    /* generic per-reference direct SSD (any shape; slow)      */
+};
+
+/* Reference-grid counts along both axes (host, pure, reading R3).
+ * Returns GBM3D_ERR_ARG if H < patch, W < patch, patch < 1 or stride < 1. */
+int gbm3d_grid_dims(int H, int W, int patch, int stride, int* n_ref_y, int* n_ref_x);
+
+/* One image.  img: device int16 [H][W]; idx/dist: device int32 [Ry][Rx][K];
+ * n_valid: device int32 [Ry][Rx] or NULL.  tau: raw SSD threshold (strict), or
+ * GBM3D_TAU_NONE; tau < 0 is GBM3D_ERR_ARG. */
+int gbm3d_block_match(const int16_t* img, int H, int W, int patch, int stride, int radius,
+                      int K, int64_t tau, int32_t* idx, int32_t* dist, int32_t* n_valid,
+                      void* stream);
+
+/* B independent images (grid.z = image): imgs [B][H][W] -> [B][Ry][Rx][K]; idx are
+ * per-image raster indices.  Byte-identical to B calls of gbm3d_block_match. */
+int gbm3d_block_match_batched(const int16_t* imgs, int B, int H, int W, int patch, int stride,
+                              int radius, int K, int64_t tau, int32_t* idx, int32_t* dist,
+                              int32_t* n_valid, void* stream);
+
+/* Row range of one image for spatial sharding (the paper processes overlapping image
+ * patches in parallel).  `slab` holds global image rows
+ * [slab_y0, slab_y0 + slab_rows) of an H x W image; the call computes reference grid rows
+ * [ref_row_begin, ref_row_end) and writes idx/dist [ref_row_end - ref_row_begin][Rx][K],
+ * n_valid [..][Rx], with GLOBAL raster indices.  The slab must contain every row those
+ * references read: [max(0, y_first - radius), min(H, y_last + radius + patch)), where
+ * y_first/y_last are the pixel rows of the first/last reference row; else GBM3D_ERR_ARG.
+ * Concatenating the outputs of row ranges is byte-identical to gbm3d_block_match. */
+int gbm3d_block_match_rows(const int16_t* slab, int slab_y0, int slab_rows, int H, int W,
+                           int patch, int stride, int radius, int K, int64_t tau,
+                           int ref_row_begin, int ref_row_end, int32_t* idx, int32_t* dist,
+                           int32_t* n_valid, void* stream);
+
+/* gbm3d_block_match_batched with an explicit method (GBM3D_METHOD_*).  B >= 1. */
+int gbm3d_block_match_ex(const int16_t* imgs, int B, int H, int W, int patch, int stride,
+                         int radius, int K, int64_t tau, int method, int32_t* idx,
+                         int32_t* dist, int32_t* n_valid, void* stream);
+
+/* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
+ * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
+ * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out
+ * on `stream`, and BLOCKS until the results are on the host. */
+size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, int K);
+int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,
+                           int radius, int K, int64_t tau, int32_t* h_idx, int32_t* h_dist,
+                           int32_t* h_n_valid, void* d_workspace, size_t workspace_bytes,
+                           void* stream);
+
+/* Range precondition (reading R10): *ok = 1 iff patch^2 * (max - min)^2 <= 2^31 - 1 over
+ * the n device int16 values at img.  BLOCKING (synchronises `stream`).  Returns
+ * GBM3D_ERR_ARG for null pointers or n < 1. */
+int gbm3d_check_range(const int16_t* img, int64_t n, int patch, int* ok, void* stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued (for the
+ * bench's gpu_launches claim). */
+int gbm3d_last_launch_count(void);
+
+/* Static string for a status code. */
+const char* gbm3d_strerror(int status);
+
+/* Library version string. */
+const char* gbm3d_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GBM3D_H */

@@ -52,6 +52,11 @@ def _load():
                 ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                 ctypes.c_int, ctypes.c_int, ctypes.c_int64, i32p, i32p, i32p, ctypes.c_int]
             lib.oracle_block_match.restype = ctypes.c_int
+            lib.oracle_block_match_refs.argtypes = [
+                ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                ctypes.c_int, ctypes.c_int, ctypes.c_int64, i32p, i32p, ctypes.c_int, i32p, i32p,
+                i32p, ctypes.c_int]
+            lib.oracle_block_match_refs.restype = ctypes.c_int
             lib.oracle_grid.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_int)]
             lib.oracle_grid.restype = ctypes.c_int
@@ -106,6 +111,30 @@ def block_match(img: np.ndarray, patch: int, stride: int, radius: int, K: int,
         raise OverflowError("a patch distance exceeds INT32_MAX (outside the int32 domain, R10)")
     if st != 0:
         raise RuntimeError(f"oracle_block_match failed: {st}")
+    return idx, dist, nv
+
+
+def block_match_refs(img: np.ndarray, patch: int, stride: int, radius: int, K: int,
+                     tau: Optional[int], py, px, threads: int = 0):
+    """The definition for selected reference grid cells (py[i], px[i]) only.
+    Returns (idx [n, K], dist [n, K], n_valid [n])."""
+    img = np.ascontiguousarray(img, dtype=np.int16)
+    H, W = img.shape
+    py = np.ascontiguousarray(py, dtype=np.int32)
+    px = np.ascontiguousarray(px, dtype=np.int32)
+    n = len(py)
+    idx = np.empty((n, K), np.int32)
+    dist = np.empty((n, K), np.int32)
+    nv = np.empty((n,), np.int32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    st = _load().oracle_block_match_refs(
+        img.ctypes.data, H, W, patch, stride, radius, K, -1 if tau is None else int(tau),
+        py.ctypes.data_as(i32p), px.ctypes.data_as(i32p), n, idx.ctypes.data_as(i32p),
+        dist.ctypes.data_as(i32p), nv.ctypes.data_as(i32p), int(threads))
+    if st == ORACLE_ERR_RANGE:
+        raise OverflowError("a patch distance exceeds INT32_MAX (outside the int32 domain, R10)")
+    if st != 0:
+        raise RuntimeError(f"oracle_block_match_refs failed: {st}")
     return idx, dist, nv
 
 

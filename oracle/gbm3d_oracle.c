@@ -168,6 +168,93 @@ int oracle_block_match(const int16_t* img, int H, int W, int P, int s, int r, in
     return status;
 }
 
+/*
+ * The same definition (steps 2-5) for an explicit list of reference grid cells (py[i], px[i]),
+ * used to check full-size GPU runs on sampled references.  Outputs are [n][K] and [n].
+ */
+int oracle_block_match_refs(const int16_t* img, int H, int W, int P, int s, int r, int K,
+                            int64_t tau, const int32_t* py_list, const int32_t* px_list, int n,
+                            int32_t* idx_out, int32_t* dist_out, int32_t* nvalid_out,
+                            int nthreads) {
+    if (!img || !idx_out || !dist_out || !py_list || !px_list || n < 0 || H < P || W < P ||
+        P < 1 || s < 1 || r < 0 || K < 1)
+        return ORACLE_ERR_ARG;
+    int Ry = oracle_grid(H, P, s, NULL), Rx = oracle_grid(W, P, s, NULL);
+    int* gy = (int*)malloc(sizeof(int) * (size_t)Ry);
+    int* gx = (int*)malloc(sizeof(int) * (size_t)Rx);
+    if (!gy || !gx) {
+        free(gy);
+        free(gx);
+        return ORACLE_ERR_NOMEM;
+    }
+    oracle_grid(H, P, s, gy);
+    oracle_grid(W, P, s, gx);
+    int status = ORACLE_OK;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic)
+    for (int t = 0; t < n; t++) {
+        if (py_list[t] < 0 || py_list[t] >= Ry || px_list[t] < 0 || px_list[t] >= Rx) {
+#pragma omp atomic write
+            status = ORACLE_ERR_ARG;
+            continue;
+        }
+        /* one-reference view: call the whole-image routine on a 1x1 grid is not possible, so
+           steps 2-5 are written out again here, literally as above */
+        const int ry = gy[py_list[t]], rx = gx[px_list[t]];
+        const int64_t self_idx = (int64_t)ry * W + rx;
+        int cy0 = ry - r < 0 ? 0 : ry - r;
+        int cy1 = ry + r > H - P ? H - P : ry + r;
+        int cx0 = rx - r < 0 ? 0 : rx - r;
+        int cx1 = rx + r > W - P ? W - P : rx + r;
+        oracle_cand* cands =
+            (oracle_cand*)malloc(sizeof(oracle_cand) * (size_t)((cy1 - cy0 + 1) * (cx1 - cx0 + 1)));
+        if (!cands) {
+#pragma omp atomic write
+            status = ORACLE_ERR_NOMEM;
+            continue;
+        }
+        int64_t m = 0;
+        for (int cy = cy0; cy <= cy1; cy++) {
+            for (int cx = cx0; cx <= cx1; cx++) {
+                if (cy == ry && cx == rx) continue;
+                int64_t d = oracle_patch_ssd(img, W, ry, rx, cy, cx, P);
+                if (d > INT32_MAX) {
+#pragma omp atomic write
+                    status = ORACLE_ERR_RANGE;
+                }
+                if (tau >= 0 && !(d < tau)) continue;
+                cands[m].d = d;
+                cands[m].idx = (int64_t)cy * W + cx;
+                m++;
+            }
+        }
+        qsort(cands, (size_t)m, sizeof(oracle_cand), oracle_cmp);
+        const int64_t base = (int64_t)t * K;
+        idx_out[base] = (int32_t)self_idx;
+        dist_out[base] = 0;
+        int nv = 1;
+        for (int k = 1; k < K; k++) {
+            if (k - 1 < m) {
+                idx_out[base + k] = (int32_t)cands[k - 1].idx;
+                dist_out[base + k] = (int32_t)cands[k - 1].d;
+                nv++;
+            } else {
+                idx_out[base + k] = (int32_t)self_idx;
+                dist_out[base + k] = -1;
+            }
+        }
+        if (nvalid_out) nvalid_out[t] = nv;
+        free(cands);
+    }
+    free(gy);
+    free(gx);
+    return status;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

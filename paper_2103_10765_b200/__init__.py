@@ -1,0 +1,222 @@
+"""B200-native block matching for G-BM3D (arXiv 2103.10765) -- Python binding of libgbm3d.so.
+
+Argument marshalling only: every step of the matching runs in the CUDA kernels of
+``libgbm3d.so`` (C ABI: ``include/gbm3d.h``).  PyTorch provides device memory and streams.
+There is no CPU fallback: if the library is missing or no CUDA device is present, the calls
+raise.  See DESIGN.md for the method (section II, Eq. (1), Prop. 1, S^K_pq).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+__all__ = [
+    "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
+    "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
+    "last_launch_count", "version",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libgbm3d.so")
+TAU_NONE = (1 << 63) - 1  # GBM3D_TAU_NONE
+METHODS = {"auto": 0, "ssd": 1, "product": 2, "direct": 3}
+_ERR = {0: "ok", -1: "GBM3D_ERR_ARG", -2: "GBM3D_ERR_RANGE", -3: "GBM3D_ERR_UNSUPPORTED",
+        -4: "GBM3D_ERR_CUDA"}
+_lib = None
+
+
+class GBM3DError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {_ERR.get(status, status)} ({_strerror(status)})")
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libgbm3d.so (built in-tree by paper_2103_10765_b200/build.py).  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: build it with "
+                          "`python -m paper_2103_10765_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i32, i64, ip = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "gbm3d_grid_dims": (i32, [i32, i32, i32, i32, ip, ip]),
+        "gbm3d_block_match": (i32, [vp, i32, i32, i32, i32, i32, i32, i64, vp, vp, vp, vp]),
+        "gbm3d_block_match_batched": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i64, vp, vp,
+                                            vp, vp]),
+        "gbm3d_block_match_rows": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i32, i64, i32,
+                                         i32, vp, vp, vp, vp]),
+        "gbm3d_block_match_ex": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i64, i32, vp, vp,
+                                       vp, vp]),
+        "gbm3d_host_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32, i32, i32, i32]),
+        "gbm3d_block_match_host": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i64, vp, vp, vp,
+                                         vp, ctypes.c_size_t, vp]),
+        "gbm3d_check_range": (i32, [vp, i64, i32, ip, vp]),
+        "gbm3d_last_launch_count": (i32, []),
+        "gbm3d_strerror": (ctypes.c_char_p, [i32]),
+        "gbm3d_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _strerror(status: int) -> str:
+    try:
+        return load_library().gbm3d_strerror(status).decode()
+    except Exception:
+        return "?"
+
+
+def version() -> str:
+    return load_library().gbm3d_version().decode()
+
+
+def last_launch_count() -> int:
+    """Kernel launches enqueued by the last successful call on this thread."""
+    return int(load_library().gbm3d_last_launch_count())
+
+
+def grid_dims(H: int, W: int, patch: int, stride: int) -> Tuple[int, int]:
+    ry, rx = ctypes.c_int(), ctypes.c_int()
+    st = load_library().gbm3d_grid_dims(H, W, patch, stride, ctypes.byref(ry), ctypes.byref(rx))
+    if st != 0:
+        raise GBM3DError(st, "grid_dims")
+    return ry.value, rx.value
+
+
+def _tau(tau: Optional[int]) -> int:
+    return TAU_NONE if tau is None else int(tau)
+
+
+def _stream_handle(device):
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check_cuda_int16(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int16:
+        raise TypeError(f"{name} must be a CUDA torch.int16 tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def check_range(img, patch: int) -> bool:
+    """P^2 (max-min)^2 <= 2^31-1 on the device (reading R10).  Synchronises the stream."""
+    _check_cuda_int16(img, "img")
+    ok = ctypes.c_int(0)
+    st = load_library().gbm3d_check_range(ctypes.c_void_p(img.data_ptr()), img.numel(), patch,
+                                          ctypes.byref(ok), _stream_handle(img.device))
+    if st != 0:
+        raise GBM3DError(st, "check_range")
+    return bool(ok.value)
+
+
+def _alloc_out(shape, device, out):
+    import torch
+    if out is not None:
+        idx, dist, nv = out
+        for t, s, n in ((idx, shape, "idx"), (dist, shape, "dist"), (nv, shape[:-1], "n_valid")):
+            if t is None and n == "n_valid":
+                continue
+            if t.dtype != torch.int32 or tuple(t.shape) != tuple(s) or not t.is_contiguous() \
+                    or t.device != device:
+                raise ValueError(f"out {n} must be contiguous int32 {tuple(s)} on {device}")
+        return idx, dist, nv
+    return (torch.empty(shape, dtype=torch.int32, device=device),
+            torch.empty(shape, dtype=torch.int32, device=device),
+            torch.empty(shape[:-1], dtype=torch.int32, device=device))
+
+
+def block_match(img, patch: int, stride: int, radius: int, K: int, tau: Optional[int] = None,
+                check: bool = True, method: str = "auto", out=None):
+    """Block matching of one image [H, W] or a batch [B, H, W] (CUDA int16).
+
+    Returns (idx, dist, n_valid) int32 CUDA tensors of shapes [(B,) Ry, Rx, K] and
+    [(B,) Ry, Rx]: slot 0 = the reference (d = 0), slots 1..n_valid-1 = the K-1 nearest
+    candidates of the clamped (2 radius + 1)^2 window by (SSD, raster index) with SSD < tau,
+    pads = (reference, -1).  Enqueued on torch's current stream.  ``check`` runs the
+    (blocking) range precondition first."""
+    _check_cuda_int16(img, "img")
+    batched = img.dim() == 3
+    if img.dim() not in (2, 3):
+        raise ValueError("img must be [H, W] or [B, H, W]")
+    B = img.shape[0] if batched else 1
+    H, W = img.shape[-2], img.shape[-1]
+    if check and not check_range(img, patch):
+        raise GBM3DError(-2, "block_match")
+    Ry, Rx = grid_dims(H, W, patch, stride)
+    shape = ((B,) if batched else ()) + (Ry, Rx, K)
+    idx, dist, nv = _alloc_out(shape, img.device, out)
+    st = load_library().gbm3d_block_match_ex(
+        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
+        METHODS[method], ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+        ctypes.c_void_p(nv.data_ptr() if nv is not None else 0), _stream_handle(img.device))
+    if st != 0:
+        raise GBM3DError(st, "block_match")
+    return idx, dist, nv
+
+
+def block_match_rows(slab, slab_y0: int, H: int, W: int, patch: int, stride: int, radius: int,
+                     K: int, tau: Optional[int], row_begin: int, row_end: int, out=None):
+    """Reference grid rows [row_begin, row_end) of an H x W image whose rows
+    [slab_y0, slab_y0 + slab.shape[0]) are in ``slab`` (spatial sharding).
+    Global raster indices; outputs [row_end-row_begin, Rx, K]."""
+    _check_cuda_int16(slab, "slab")
+    if slab.dim() != 2 or slab.shape[1] != W:
+        raise ValueError("slab must be [rows, W]")
+    _, Rx = grid_dims(H, W, patch, stride)
+    idx, dist, nv = _alloc_out((row_end - row_begin, Rx, K), slab.device, out)
+    st = load_library().gbm3d_block_match_rows(
+        ctypes.c_void_p(slab.data_ptr()), slab_y0, slab.shape[0], H, W, patch, stride, radius, K,
+        _tau(tau), row_begin, row_end, ctypes.c_void_p(idx.data_ptr()),
+        ctypes.c_void_p(dist.data_ptr()), ctypes.c_void_p(nv.data_ptr() if nv is not None else 0),
+        _stream_handle(slab.device))
+    if st != 0:
+        raise GBM3DError(st, "block_match_rows")
+    return idx, dist, nv
+
+
+def host_workspace_bytes(B: int, H: int, W: int, patch: int, stride: int, K: int) -> int:
+    return int(load_library().gbm3d_host_workspace_bytes(B, H, W, patch, stride, K))
+
+
+def block_match_host(h_img, patch: int, stride: int, radius: int, K: int,
+                     tau: Optional[int] = None, workspace=None, out=None, device=None):
+    """End-to-end entry: host (ideally pinned) int16 [B, H, W] torch tensor in, host int32
+    tables out; the library copies in, matches and copies out, blocking until done."""
+    import torch
+    if h_img.device.type != "cpu" or h_img.dtype != torch.int16 or not h_img.is_contiguous():
+        raise TypeError("h_img must be a contiguous CPU torch.int16 tensor")
+    x = h_img if h_img.dim() == 3 else h_img.unsqueeze(0)
+    B, H, W = x.shape
+    Ry, Rx = grid_dims(H, W, patch, stride)
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    need = host_workspace_bytes(B, H, W, patch, stride, K)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=device)
+    if out is None:
+        pin = torch.cuda.is_available()
+        out = (torch.empty((B, Ry, Rx, K), dtype=torch.int32, pin_memory=pin),
+               torch.empty((B, Ry, Rx, K), dtype=torch.int32, pin_memory=pin),
+               torch.empty((B, Ry, Rx), dtype=torch.int32, pin_memory=pin))
+    idx, dist, nv = out
+    st = load_library().gbm3d_block_match_host(
+        ctypes.c_void_p(x.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
+        ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+        ctypes.c_void_p(nv.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+        _stream_handle(device))
+    if st != 0:
+        raise GBM3DError(st, "block_match_host")
+    return out

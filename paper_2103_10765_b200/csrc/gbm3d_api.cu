@@ -1,0 +1,289 @@
+// C ABI of libgbm3d.so (include/gbm3d.h): argument validation, grid geometry, kernel dispatch.
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
+
+#include "../../include/gbm3d.h"
+#include "common.cuh"
+#include "match_direct.cuh"
+#include "match_strip.cuh"
+
+namespace gbm3d {
+
+static thread_local int g_last_launches = 0;
+
+// Fast-path table: (patch, stride) pairs with an instantiated strip kernel.
+static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok) {
+    *ok = true;
+    switch (p.P * 100 + p.S) {
+        case 803: return launch_strip<StripCfg<8, 3, 8, 5>>(p, st, launches);
+        case 1204: return launch_strip<StripCfg<12, 4, 4, 4>>(p, st, launches);
+        case 802: return launch_strip<StripCfg<8, 2, 8, 5>>(p, st, launches);
+        case 804: return launch_strip<StripCfg<8, 4, 6, 4>>(p, st, launches);
+        default: *ok = false; return cudaSuccess;
+    }
+}
+
+static int grid_count(int L, int P, int S) { return (L - P) / S + 1 + (((L - P) % S) ? 1 : 0); }
+
+static int ceil_log2(long long v) {
+    int b = 0;
+    while ((1LL << b) < v) ++b;
+    return b;
+}
+
+// Validate and fill the launch parameters shared by every entry point.
+static int make_params(MatchParams& p, int B, int H, int W, int patch, int stride, int radius,
+                       int K, int64_t tau) {
+    if (B < 1 || H < 1 || W < 1 || patch < 1 || stride < 1 || radius < 0 || K < 1 || tau < 0)
+        return GBM3D_ERR_ARG;
+    if (H < patch || W < patch) return GBM3D_ERR_ARG;
+    if ((long long)H * (long long)W >= (1LL << 31)) return GBM3D_ERR_ARG;
+    if (patch > 16 || radius > 32 || K > 64) return GBM3D_ERR_UNSUPPORTED;
+    p = MatchParams{};
+    p.B = B;
+    p.H = H;
+    p.W = W;
+    p.P = patch;
+    p.S = stride;
+    p.r = radius;
+    p.K = K;
+    p.tau = tau;
+    p.Ry = grid_count(H, patch, stride);
+    p.Rx = grid_count(W, patch, stride);
+    p.Ry_reg = (H - patch) / stride + 1;
+    p.Rx_reg = (W - patch) / stride + 1;
+    p.img_bstride = (int64_t)H * W;
+    p.out_bstride = (int64_t)p.Ry * p.Rx;
+    p.slab_y0 = 0;
+    p.slab_y1 = H;
+    p.row_begin = 0;
+    p.row_end = p.Ry;
+    p.side = 2 * radius + 1;
+    p.cb = ceil_log2((long long)p.side * p.side + 1);
+    p.dsat = (uint32_t)((1ULL << (32 - p.cb)) - 1ULL);
+    const int64_t taum1 = tau - 1;  // strict: d < tau  <=>  d <= tau - 1
+    p.tdr0 = (int)(taum1 < (int64_t)p.dsat ? taum1 : (int64_t)p.dsat);
+    p.thr0 = (tau <= (int64_t)p.dsat) ? (uint32_t)((uint64_t)tau << p.cb) : KEY_INF;
+    p.tau_above_dsat = taum1 > (int64_t)p.dsat ? 1 : 0;
+    return GBM3D_OK;
+}
+
+static cudaError_t launch_direct(const MatchParams& p, cudaStream_t st, int k_begin, int k_end,
+                                 int m_begin, int m_end, int* launches) {
+    if (k_end <= k_begin || m_end <= m_begin) return cudaSuccess;
+    const long long wy = std::min(p.side, p.H - p.P + 1), wx = std::min(p.side, p.W - p.P + 1);
+    int npow2 = 1;
+    while (npow2 < wy * wx) npow2 <<= 1;
+    if (npow2 < 2) npow2 = 2;
+    const int smem = npow2 * 8;
+    cudaError_t e = cudaFuncSetAttribute(match_direct_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const long long nref = (long long)(k_end - k_begin) * (m_end - m_begin);
+    dim3 grid((unsigned)nref, 1, p.B);
+    match_direct_kernel<<<grid, 256, smem, st>>>(p, k_begin, m_begin, m_end - m_begin, npow2);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+// Dispatch one call: strip kernel over the regular grid part, direct kernel for the appended
+// row/column (reading R3), or direct for everything when no fast kernel fits.
+static int run(const MatchParams& p, int method, cudaStream_t st) {
+    int launches = 0;
+    cudaError_t e = cudaSuccess;
+    bool fast = false;
+    if (method == GBM3D_METHOD_PRODUCT) return GBM3D_ERR_UNSUPPORTED;
+    if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_SSD) {
+        e = strip_dispatch(p, st, &launches, &fast);
+        if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (!fast && method == GBM3D_METHOD_SSD) return GBM3D_ERR_UNSUPPORTED;
+    }
+    if (fast) {
+        const int kr1 = std::min(p.row_end, p.Ry_reg);
+        // appended column for the regular rows of the call
+        if (p.Rx > p.Rx_reg) e = launch_direct(p, st, p.row_begin, kr1, p.Rx_reg, p.Rx, &launches);
+        // appended row (all columns) when it is inside the call's row range
+        if (e == cudaSuccess && p.Ry > p.Ry_reg && p.row_end > p.Ry_reg)
+            e = launch_direct(p, st, std::max(p.row_begin, p.Ry_reg), p.row_end, 0, p.Rx, &launches);
+    } else {
+        e = launch_direct(p, st, p.row_begin, p.row_end, 0, p.Rx, &launches);
+    }
+    if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+    g_last_launches = launches;
+    return GBM3D_OK;
+}
+
+// ---- range precondition (reading R10)
+__global__ void range_minmax_kernel(const int16_t* __restrict__ img, int64_t n, int* out) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = img[i];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
+}  // namespace gbm3d
+
+using namespace gbm3d;
+
+extern "C" {
+
+int gbm3d_grid_dims(int H, int W, int patch, int stride, int* n_ref_y, int* n_ref_x) {
+    if (patch < 1 || stride < 1 || H < patch || W < patch) return GBM3D_ERR_ARG;
+    if (n_ref_y) *n_ref_y = grid_count(H, patch, stride);
+    if (n_ref_x) *n_ref_x = grid_count(W, patch, stride);
+    return GBM3D_OK;
+}
+
+int gbm3d_block_match_ex(const int16_t* imgs, int B, int H, int W, int patch, int stride,
+                         int radius, int K, int64_t tau, int method, int32_t* idx,
+                         int32_t* dist, int32_t* n_valid, void* stream) {
+    if (!imgs || !idx || !dist) return GBM3D_ERR_ARG;
+    if (method < GBM3D_METHOD_AUTO || method > GBM3D_METHOD_DIRECT) return GBM3D_ERR_ARG;
+    MatchParams p;
+    const int st = make_params(p, B, H, W, patch, stride, radius, K, tau);
+    if (st != GBM3D_OK) return st;
+    p.img = imgs;
+    p.idx = idx;
+    p.dist = dist;
+    p.nvalid = n_valid;
+    return run(p, method, (cudaStream_t)stream);
+}
+
+int gbm3d_block_match(const int16_t* img, int H, int W, int patch, int stride, int radius, int K,
+                      int64_t tau, int32_t* idx, int32_t* dist, int32_t* n_valid, void* stream) {
+    return gbm3d_block_match_ex(img, 1, H, W, patch, stride, radius, K, tau, GBM3D_METHOD_AUTO,
+                                idx, dist, n_valid, stream);
+}
+
+int gbm3d_block_match_batched(const int16_t* imgs, int B, int H, int W, int patch, int stride,
+                              int radius, int K, int64_t tau, int32_t* idx, int32_t* dist,
+                              int32_t* n_valid, void* stream) {
+    return gbm3d_block_match_ex(imgs, B, H, W, patch, stride, radius, K, tau, GBM3D_METHOD_AUTO,
+                                idx, dist, n_valid, stream);
+}
+
+int gbm3d_block_match_rows(const int16_t* slab, int slab_y0, int slab_rows, int H, int W,
+                           int patch, int stride, int radius, int K, int64_t tau,
+                           int ref_row_begin, int ref_row_end, int32_t* idx, int32_t* dist,
+                           int32_t* n_valid, void* stream) {
+    if (!slab || !idx || !dist) return GBM3D_ERR_ARG;
+    MatchParams p;
+    const int st = make_params(p, 1, H, W, patch, stride, radius, K, tau);
+    if (st != GBM3D_OK) return st;
+    if (ref_row_begin < 0 || ref_row_end > p.Ry || ref_row_begin >= ref_row_end)
+        return GBM3D_ERR_ARG;
+    if (slab_y0 < 0 || slab_rows < 1 || slab_y0 + slab_rows > H) return GBM3D_ERR_ARG;
+    const int y_first = grid_pos(ref_row_begin, p.Ry_reg, stride, H - patch);
+    const int y_last = grid_pos(ref_row_end - 1, p.Ry_reg, stride, H - patch);
+    const int need0 = std::max(0, y_first - radius);
+    const int need1 = std::min(H, y_last + radius + patch);
+    if (slab_y0 > need0 || slab_y0 + slab_rows < need1) return GBM3D_ERR_ARG;
+    p.img = slab;
+    p.slab_y0 = slab_y0;
+    p.slab_y1 = slab_y0 + slab_rows;
+    p.row_begin = ref_row_begin;
+    p.row_end = ref_row_end;
+    p.idx = idx;
+    p.dist = dist;
+    p.nvalid = n_valid;
+    p.out_bstride = (int64_t)(ref_row_end - ref_row_begin) * p.Rx;
+    return run(p, GBM3D_METHOD_AUTO, (cudaStream_t)stream);
+}
+
+size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, int K) {
+    if (B < 1 || patch < 1 || stride < 1 || H < patch || W < patch || K < 1) return 0;
+    const size_t img = ((size_t)B * H * W * 2 + 255) & ~(size_t)255;
+    const size_t nref = (size_t)B * grid_count(H, patch, stride) * grid_count(W, patch, stride);
+    const size_t tab = (nref * K * 4 + 255) & ~(size_t)255;
+    const size_t nv = (nref * 4 + 255) & ~(size_t)255;
+    return img + 2 * tab + nv;
+}
+
+int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,
+                           int radius, int K, int64_t tau, int32_t* h_idx, int32_t* h_dist,
+                           int32_t* h_n_valid, void* d_workspace, size_t workspace_bytes,
+                           void* stream) {
+    if (!h_imgs || !h_idx || !h_dist || !d_workspace) return GBM3D_ERR_ARG;
+    const size_t need = gbm3d_host_workspace_bytes(B, H, W, patch, stride, K);
+    if (need == 0 || workspace_bytes < need) return GBM3D_ERR_ARG;
+    MatchParams p;
+    int st = make_params(p, B, H, W, patch, stride, radius, K, tau);
+    if (st != GBM3D_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = (char*)d_workspace;
+    const size_t img_b = (size_t)B * H * W * 2;
+    const size_t nref = (size_t)B * p.Ry * p.Rx;
+    int16_t* d_img = (int16_t*)ws;
+    int32_t* d_idx = (int32_t*)(ws + ((img_b + 255) & ~(size_t)255));
+    int32_t* d_dist = (int32_t*)((char*)d_idx + ((nref * K * 4 + 255) & ~(size_t)255));
+    int32_t* d_nv = (int32_t*)((char*)d_dist + ((nref * K * 4 + 255) & ~(size_t)255));
+    if (cudaMemcpyAsync(d_img, h_imgs, img_b, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return GBM3D_ERR_CUDA;
+    p.img = d_img;
+    p.idx = d_idx;
+    p.dist = d_dist;
+    p.nvalid = d_nv;
+    st = run(p, GBM3D_METHOD_AUTO, s);
+    if (st != GBM3D_OK) return st;
+    if (cudaMemcpyAsync(h_idx, d_idx, nref * K * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return GBM3D_ERR_CUDA;
+    if (cudaMemcpyAsync(h_dist, d_dist, nref * K * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return GBM3D_ERR_CUDA;
+    if (h_n_valid &&
+        cudaMemcpyAsync(h_n_valid, d_nv, nref * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return GBM3D_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return GBM3D_ERR_CUDA;
+    return GBM3D_OK;
+}
+
+int gbm3d_check_range(const int16_t* img, int64_t n, int patch, int* ok, void* stream) {
+    if (!img || !ok || n < 1 || patch < 1) return GBM3D_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    int* d = nullptr;
+    if (cudaMallocAsync((void**)&d, 2 * sizeof(int), s) != cudaSuccess) return GBM3D_ERR_CUDA;
+    const int init[2] = {INT_MAX, INT_MIN};
+    int h[2];
+    cudaError_t e = cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+        range_minmax_kernel<<<blocks, 256, 0, s>>>(img, n, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+    const long long span = (long long)h[1] - (long long)h[0];
+    *ok = ((long long)patch * patch * span * span <= (long long)INT32_MAX) ? 1 : 0;
+    return GBM3D_OK;
+}
+
+int gbm3d_last_launch_count(void) { return g_last_launches; }
+
+const char* gbm3d_strerror(int status) {
+    switch (status) {
+        case GBM3D_OK: return "ok";
+        case GBM3D_ERR_ARG: return "invalid argument";
+        case GBM3D_ERR_RANGE: return "image range violates patch^2*(max-min)^2 <= 2^31-1";
+        case GBM3D_ERR_UNSUPPORTED: return "unsupported size (patch > 16, radius > 32, K > 64, or method)";
+        case GBM3D_ERR_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+const char* gbm3d_version(void) { return "gbm3d 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,466 @@
+// Fast exact block-matching kernel, organised by search displacement (SSD form).
+//
+// Method (section II): for a fixed displacement delta = (dy, dx) the distance of every
+// reference rho on the strided grid is the P x P box sum of the shifted-difference image
+//     e_delta(y, x) = (Z[y][x] - Z[y+dy][x+dx])^2                          (Eq. (1))
+// i.e. Prop. 1 with an all-ones block applied to e_delta, the box-filter step
+// of PAPER.md:113.  The box sum is separable: vertical sums at reference rows, then horizontal
+// sums at reference columns.  Everything is exact int32 arithmetic (reading R10).
+//
+// Work mapping:
+//   * CTA = NS strips stacked vertically, two warps per strip.  The CTA stages its image region
+//     (tile + radius halo) into shared memory once, as int16, zero outside the image.
+//   * strip = RC = 32 - HL reference columns x TRY reference rows.  Lane l of both warps of the
+//     strip owns the S pixel columns of reference column m0+l and keeps that column strip's
+//     pixels (NR rows x S) in registers for the whole kernel (the "a" side of every difference).
+//   * displacements are visited in blocks of D consecutive dy at one dx; the two warps of a strip
+//     take alternate blocks.  For one block a lane streams the NR + D - 1 shifted rows ("b" side)
+//     from shared memory once; each shifted row feeds D displacements (register reuse across dy).
+//   * vertical box sums per column use chunk sums of S rows (C) and of the first P%S rows (A):
+//       V_k = C_k + ... + C_{k+Q-1} + A_{k+Q},   Q = P / S,
+//     horizontal sums combine the lane's column sums with Q neighbouring lanes via shuffles.
+//   * selection (arg_K min): per reference a max-heap of the K-1 smallest 32-bit
+//     keys (d << cb | code) in shared memory, shared by the strip's two warps.  The per-eval
+//     gate is one compare against a register copy of the heap root; passing candidates go to a
+//     per-(warp, ref) queue with predicated stores.  After each pair of blocks the warps merge
+//     both queues into the heaps (each warp owns half of the reference rows), then refresh the
+//     gates.  At the end an in-place heapsort orders each heap and the strip writes the tables
+//     with coalesced 128-byte rows.
+#pragma once
+#include "common.cuh"
+
+namespace gbm3d {
+
+constexpr int HEAP_STRIDE = 33;  // words per heap row: conflict-free per-lane AND per-ref access
+
+template <int P_, int S_, int TRY_, int D_>
+struct StripCfg {
+    static constexpr int P = P_, S = S_, TRY = TRY_, D = D_;
+    static constexpr int Q = P / S, REM = P % S;
+    static constexpr int HL = (P + S - 1) / S - 1;       // helper lanes (no references)
+    static constexpr int RC = 32 - HL;                   // reference columns per warp
+    static constexpr int NR = S * (TRY - 1) + P;         // pixel rows of a strip
+    static constexpr int NCH = TRY - 1 + Q + (REM > 0);  // row chunks of a strip
+    static constexpr int COLS = 32 * S;                  // pixel columns covered by a warp
+    static_assert(S <= P, "fast path needs stride <= patch");
+    static_assert(TRY % 2 == 0, "the two warps of a strip split the reference rows");
+};
+
+// Shared-memory geometry of one CTA (host and device agree on it).
+struct StripSmem {
+    int pitch, rows, img_bytes, heap_words, queue_words, count_bytes;
+    __host__ __device__ static StripSmem make(int COLS, int S, int P, int TRY, int D, int NS, int r,
+                                              int K) {
+        StripSmem g;
+        g.pitch = (COLS + 2 * r + 1) & ~1;
+        g.rows = S * (TRY * NS - 1) + P + 2 * r + (D - 1);  // + D-1 rows read by the dy tail block
+        g.img_bytes = ((g.rows * g.pitch * 2) + 15) & ~15;
+        g.heap_words = NS * TRY * (K - 1) * HEAP_STRIDE;
+        g.queue_words = 2 * NS * TRY * D * 32;
+        g.count_bytes = 2 * NS * TRY * 32;
+        return g;
+    }
+    __host__ __device__ int bytes() const {
+        return img_bytes + 4 * (heap_words + queue_words) + ((count_bytes + 15) & ~15);
+    }
+};
+
+// Max-heap of n keys at H[i * HEAP_STRIDE]: replace the root by key (key < root) and sift down.
+static __device__ __forceinline__ void heap_replace_root(uint32_t* H, int n, uint32_t key) {
+    int i = 0;
+    for (;;) {
+        const int c = 2 * i + 1;
+        if (c >= n) break;
+        const uint32_t v1 = H[c * HEAP_STRIDE];
+        const uint32_t v2 = (c + 1 < n) ? H[(c + 1) * HEAP_STRIDE] : 0u;
+        const bool right = v2 > v1;
+        const uint32_t big = right ? v2 : v1;
+        if (big < key) break;  // keys are unique
+        H[i * HEAP_STRIDE] = big;
+        i = right ? c + 1 : c;
+    }
+    H[i * HEAP_STRIDE] = key;
+}
+
+// In-place heapsort of a max-heap of n keys -> ascending order.
+static __device__ void heap_sort(uint32_t* H, int n) {
+    for (int end = n - 1; end > 0; --end) {
+        const uint32_t top = H[0];
+        const uint32_t key = H[end * HEAP_STRIDE];
+        H[end * HEAP_STRIDE] = top;
+        int i = 0;
+        for (;;) {
+            const int c = 2 * i + 1;
+            if (c >= end) break;
+            const uint32_t v1 = H[c * HEAP_STRIDE];
+            const uint32_t v2 = (c + 1 < end) ? H[(c + 1) * HEAP_STRIDE] : 0u;
+            const bool right = v2 > v1;
+            const uint32_t big = right ? v2 : v1;
+            if (big <= key) break;
+            H[i * HEAP_STRIDE] = big;
+            i = right ? c + 1 : c;
+        }
+        H[i * HEAP_STRIDE] = key;
+    }
+}
+
+static __device__ __forceinline__ void pair_sync(int strip) {
+    asm volatile("bar.sync %0, 64;" ::"r"(strip + 1) : "memory");
+}
+
+// One displacement block: D consecutive dy at a fixed dx, all TRY reference rows of the lane.
+template <class Cfg, bool MASKED>
+__device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, int pitch, int brow,
+                                            int bcol, const int (&a)[Cfg::NR][Cfg::S],
+                                            const int (&tdr)[Cfg::TRY], uint32_t* (&qp)[Cfg::TRY],
+                                            const uint32_t (&mk)[Cfg::TRY], uint32_t code0,
+                                            uint32_t side, uint32_t mulcb) {
+    constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
+    constexpr int Q = Cfg::Q, REM = Cfg::REM, NCH = Cfg::NCH;
+    int Cc[D][NCH][S];
+    int Ac[D][NCH][S];
+#pragma unroll
+    for (int t = 0; t < NR + D - 1; ++t) {
+        int bv[S];
+        const int16_t* rowp = sm_img + (brow + t) * pitch + bcol;
+#pragma unroll
+        for (int c = 0; c < S; ++c) bv[c] = rowp[c];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const int y = t - j;
+            if (y < 0 || y >= NR) continue;
+            const int ch = y / S, pos = y % S;
+#pragma unroll
+            for (int c = 0; c < S; ++c) {
+                const int df = a[y][c] - bv[c];
+                if (pos == 0)
+                    Cc[j][ch][c] = df * df;
+                else
+                    Cc[j][ch][c] += df * df;
+                if (REM > 0 && pos == REM - 1) Ac[j][ch][c] = Cc[j][ch][c];
+            }
+            // reference row k is complete once its last pixel row y = S k + P - 1 is in
+            if (y >= P - 1 && (y - (P - 1)) % S == 0 && (y - (P - 1)) / S < TRY) {
+                const int k = (y - (P - 1)) / S;
+                int hc = 0, ha = 0;
+#pragma unroll
+                for (int c = 0; c < S; ++c) {
+                    int v = 0;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) v += Cc[j][k + q][c];
+                    if (REM > 0) v += Ac[j][k + Q][c];
+                    if (c < REM) ha += v;
+                    hc += v;
+                }
+                int d = hc;
+#pragma unroll
+                for (int q = 1; q < Q; ++q) d += __shfl_down_sync(0xffffffffu, hc, q);
+                if (REM > 0) d += __shfl_down_sync(0xffffffffu, ha, Q);
+                bool pass = d <= tdr[k];
+                if (MASKED) pass = pass && ((mk[k] >> j) & 1u);
+                if (pass) {
+                    *qp[k] = (uint32_t)d * mulcb + (code0 + (uint32_t)j * side);
+                    qp[k] += 32;
+                }
+            }
+        }
+    }
+}
+
+// Exact per-reference recomputation with 64-bit keys, used only for references whose 32-bit
+// key range may have dropped a valid candidate (tau - 1 > dsat and the heap is not full).
+// The list lives directly in the output slots 1..K-1.  Returns the number of matches.
+static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ sm_img, int pitch,
+                                                   int sy, int sx, int ry, int rx,
+                                                   const MatchParams& p, int32_t* oi,
+                                                   int32_t* od) {
+    const int L = p.K - 1, P = p.P, r = p.r;
+    int cnt = 0;
+    const int cy0 = max(0, ry - r), cy1 = min(p.H - P, ry + r);
+    const int cx0 = max(0, rx - r), cx1 = min(p.W - P, rx + r);
+    for (int cy = cy0; cy <= cy1; ++cy) {
+        for (int cx = cx0; cx <= cx1; ++cx) {
+            if (cy == ry && cx == rx) continue;
+            int64_t d = 0;
+            for (int i = 0; i < P; ++i) {
+                const int16_t* ra = sm_img + (sy + i) * pitch + sx;
+                const int16_t* rb = sm_img + (sy + cy - ry + i) * pitch + sx + (cx - rx);
+                for (int jj = 0; jj < P; ++jj) {
+                    const int64_t df = (int64_t)ra[jj] - (int64_t)rb[jj];
+                    d += df * df;
+                }
+            }
+            if (d >= p.tau) continue;
+            const uint64_t key = ((uint64_t)d << 32) | (uint32_t)(cy * p.W + cx);
+            int pos;
+            if (cnt < L) {
+                pos = cnt++;
+            } else {
+                const uint64_t last = ((uint64_t)(uint32_t)od[L] << 32) | (uint32_t)oi[L];
+                if (key >= last) continue;
+                pos = L - 1;
+            }
+            while (pos > 0) {
+                const uint64_t prev = ((uint64_t)(uint32_t)od[pos] << 32) | (uint32_t)oi[pos];
+                if (prev < key) break;
+                od[pos + 1] = od[pos];
+                oi[pos + 1] = oi[pos];
+                --pos;
+            }
+            od[pos + 1] = (int32_t)d;
+            oi[pos + 1] = cy * p.W + cx;
+        }
+    }
+    const int self = ry * p.W + rx;
+    oi[0] = self;
+    od[0] = 0;
+    for (int i = cnt; i < L; ++i) {
+        oi[1 + i] = self;
+        od[1 + i] = -1;
+    }
+    return cnt;
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS) {
+    constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
+    constexpr int RC = Cfg::RC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int r = p.r;
+    const int L = p.K - 1;
+    const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K);
+    int16_t* sm_img = reinterpret_cast<int16_t*>(smem_raw);
+    uint32_t* sm_heap = reinterpret_cast<uint32_t*>(smem_raw + g.img_bytes);
+    uint32_t* sm_q = sm_heap + g.heap_words;
+    uint8_t* sm_cnt = reinterpret_cast<uint8_t*>(sm_q + g.queue_words);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int strip = warp >> 1, half = warp & 1;
+    const int b = blockIdx.z;
+    const int kr0 = p.row_begin, kr1 = min(p.row_end, p.Ry_reg);  // regular rows in this call
+    const int k0 = kr0 + (int)blockIdx.y * TRY * NS;
+    const int m0 = (int)blockIdx.x * RC;
+    const int16_t* __restrict__ img = p.img + (int64_t)b * p.img_bstride;
+
+    // ---- stage tile + halo (int16, zero outside the image / slab) and reset the heaps
+    {
+        const int gy0 = S * k0 - r, gx0 = S * m0 - r;
+        const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
+        for (int yy = warp; yy < g.rows; yy += blockDim.x >> 5) {
+            const int gy = gy0 + yy;
+            const bool rowok = gy >= ylo && gy < yhi;
+            const int16_t* src = img + (int64_t)(gy - p.slab_y0) * p.W;
+            for (int xx = lane; xx < g.pitch; xx += 32) {
+                const int gx = gx0 + xx;
+                sm_img[yy * g.pitch + xx] = (rowok && gx >= 0 && gx < p.W) ? src[gx] : (int16_t)0;
+            }
+        }
+        for (int i = threadIdx.x; i < g.heap_words; i += blockDim.x) sm_heap[i] = KEY_INF;
+    }
+    __syncthreads();
+
+    const int kw = k0 + TRY * strip;  // first reference row of this strip
+    const int m = m0 + lane;
+    const int nk = min(TRY, kr1 - kw);
+    const int nm = min(RC, p.Rx_reg - m0);
+    if (nk <= 0 || nm <= 0) return;  // strip without references (only pair barriers follow)
+    const bool lane_ok = (lane < RC) && (m < p.Rx_reg);
+
+    const int arow0 = r + S * TRY * strip;  // smem row of strip row 0
+    int a[NR][S];
+#pragma unroll
+    for (int y = 0; y < NR; ++y)
+#pragma unroll
+        for (int c = 0; c < S; ++c) a[y][c] = sm_img[(arow0 + y) * g.pitch + r + S * lane + c];
+
+    uint32_t* const heap0 = sm_heap + (strip * TRY) * L * HEAP_STRIDE + lane;  // + k*L*33
+    uint32_t* const qw = sm_q + (warp * TRY * D) * 32 + lane;                 // own queues
+    uint32_t* const qo = sm_q + ((warp ^ 1) * TRY * D) * 32 + lane;           // partner's
+    uint8_t* const cw = sm_cnt + (warp * TRY) * 32 + lane;
+    uint8_t* const co = sm_cnt + ((warp ^ 1) * TRY) * 32 + lane;
+
+    int tdr[TRY];
+    bool refok[TRY];
+    uint32_t* qp[TRY];
+#pragma unroll
+    for (int k = 0; k < TRY; ++k) {
+        refok[k] = lane_ok && (k < nk) && (L > 0);
+        tdr[k] = refok[k] ? p.tdr0 : -1;
+        qp[k] = qw + k * D * 32;
+    }
+    const int ry_first = S * kw, ry_last = S * (kw + nk - 1);
+    const int rx_first = S * m0, rx_last = S * (m0 + nm - 1);
+    const int ylast = p.H - P, xlast = p.W - P;
+    const uint32_t side = (uint32_t)p.side, mulcb = 1u << p.cb;
+    const int nDY = (p.side + D - 1) / D;
+    const int NB = p.side * nDY;  // displacement blocks (dx-major)
+
+    if (L > 0) {
+        for (int it = 0; it < NB; it += 2) {
+            const int blk = it + half;
+            if (blk < NB) {
+                const int dx = -r + blk / nDY;
+                const int dy0 = -r + (blk % nDY) * D;
+                const bool xvalid = (S * m + dx >= 0) && (S * m + dx <= xlast);
+                const bool colx_ok = (rx_first + dx >= 0) && (rx_last + dx <= xlast);
+                const int bcol = r + S * lane + dx;
+                const int brow = arow0 + dy0;
+                const uint32_t code0 = (uint32_t)((dy0 + r) * p.side + (dx + r));
+                const bool unmasked = colx_ok && (ry_first + dy0 >= 0) &&
+                                      (ry_last + dy0 + D - 1 <= ylast) && (dy0 + D - 1 <= r) &&
+                                      !(dx == 0 && dy0 <= 0 && dy0 + D > 0);
+                uint32_t mk[TRY];
+                if (unmasked) {
+#pragma unroll
+                    for (int k = 0; k < TRY; ++k) mk[k] = 0xffffffffu;
+                    strip_block<Cfg, false>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0,
+                                            side, mulcb);
+                } else {
+                    uint32_t jx = 0;
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        const int dy = dy0 + j;
+                        const bool ok = (dy <= r) && !(dx == 0 && dy == 0) && xvalid;
+                        jx |= (ok ? 1u : 0u) << j;
+                    }
+#pragma unroll
+                    for (int k = 0; k < TRY; ++k) {
+                        const int ry = S * (kw + k);
+                        const int lo = max(-(ry + dy0), 0), hi = min(ylast - ry - dy0, D - 1);
+                        const uint32_t ym =
+                            hi >= lo ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+                        mk[k] = jx & ym;
+                    }
+                    strip_block<Cfg, true>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0,
+                                           side, mulcb);
+                }
+            }
+            // publish queue lengths, then merge: this warp owns reference rows k = half (mod 2)
+#pragma unroll
+            for (int k = 0; k < TRY; ++k) {
+                cw[k * 32] = (uint8_t)((qp[k] - (qw + k * D * 32)) >> 5);
+                qp[k] = qw + k * D * 32;
+            }
+            pair_sync(strip);
+#pragma unroll
+            for (int k = half; k < TRY; k += 2) {
+                uint32_t* const H = heap0 + k * L * HEAP_STRIDE;
+                uint32_t thr = min(H[0], p.thr0);
+#pragma unroll
+                for (int src = 0; src < 2; ++src) {
+                    const uint32_t* qk = (src ? qo : qw) + k * D * 32;
+                    const int n = (src ? co : cw)[k * 32];
+                    for (int i = 0; i < n; ++i) {
+                        const uint32_t key = qk[i * 32];
+                        if (key < thr) {
+                            heap_replace_root(H, L, key);
+                            thr = min(H[0], p.thr0);
+                        }
+                    }
+                }
+            }
+            pair_sync(strip);
+#pragma unroll
+            for (int k = 0; k < TRY; ++k) {
+                if (refok[k]) {
+                    const uint32_t thr = min(heap0[k * L * HEAP_STRIDE], p.thr0);
+                    tdr[k] = thr == p.thr0 ? p.tdr0 : (int)(thr >> p.cb);
+                }
+            }
+        }
+        // ---- order each heap ascending (in place), each warp its own reference rows
+#pragma unroll 1
+        for (int k = half; k < TRY; k += 2)
+            if (refok[k]) heap_sort(heap0 + k * L * HEAP_STRIDE, L);
+        pair_sync(strip);
+    }
+
+    // ---- epilogue: coalesced rows; slot 0 = self (d = 0), ranks 1.. sorted keys, pads (self,-1)
+    const uint32_t cmask = (1u << p.cb) - 1u;
+#pragma unroll 1
+    for (int k = half; k < nk; k += 2) {
+        const int kk = kw + k, ry = S * kk;
+        const uint32_t* Hk = sm_heap + (strip * TRY + k) * L * HEAP_STRIDE;
+#pragma unroll 1
+        for (int l = 0; l < nm; ++l) {
+            const int rx = S * (m0 + l);
+            const int64_t ref =
+                (int64_t)b * p.out_bstride + (int64_t)(kk - p.row_begin) * p.Rx + (m0 + l);
+            int32_t* oi = p.idx + ref * p.K;
+            int32_t* od = p.dist + ref * p.K;
+            const int self = ry * p.W + rx;
+            int cnt = 0;
+            for (int s0 = 0; s0 < p.K; s0 += 32) {
+                const int s = s0 + lane;
+                uint32_t key = KEY_INF;
+                if (s >= 1 && s < p.K) key = Hk[(s - 1) * HEAP_STRIDE + l];
+                cnt += __popc(__ballot_sync(0xffffffffu, key != KEY_INF));
+                if (s < p.K) {
+                    int32_t vi = self, vd = (s == 0) ? 0 : -1;
+                    if (key != KEY_INF) {
+                        const uint32_t code = key & cmask;
+                        vi = (ry + (int)(code / side) - r) * p.W + rx + (int)(code % side) - r;
+                        vd = (int32_t)(key >> p.cb);
+                    }
+                    oi[s] = vi;
+                    od[s] = vd;
+                }
+            }
+            if (p.tau_above_dsat && cnt < L) {
+                const int wy = min(ylast, ry + r) - max(0, ry - r) + 1;
+                const int wx = min(xlast, rx + r) - max(0, rx - r) + 1;
+                if (cnt < wy * wx - 1) {
+                    __syncwarp();
+                    if (lane == 0)
+                        cnt = strip_exact_ref(sm_img, g.pitch, arow0 + S * k, r + S * l, ry, rx, p,
+                                              oi, od);
+                    cnt = __shfl_sync(0xffffffffu, cnt, 0);
+                }
+            }
+            if (p.nvalid && lane == 0) p.nvalid[ref] = 1 + cnt;
+        }
+    }
+}
+
+// Host launcher: picks the strips per CTA (1 or 2; two warps each) that maximise resident
+// warps per SM under the shared-memory budget, then launches over the regular grid rows.
+template <class Cfg>
+cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launches) {
+    const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
+    if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
+    int dev = 0, max_optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    auto kern = match_strip_kernel<Cfg>;
+    int best_ns = 0, best_warps = -1, best_smem = 0;
+    for (int ns : {2, 1}) {
+        const int smem =
+            StripSmem::make(Cfg::COLS, Cfg::S, Cfg::P, Cfg::TRY, Cfg::D, ns, p.r, p.K).bytes();
+        if (smem > max_optin) continue;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 64 * ns, smem);
+        if (e != cudaSuccess) return e;
+        if (nb * 2 * ns > best_warps) {
+            best_warps = nb * 2 * ns;
+            best_ns = ns;
+            best_smem = smem;
+        }
+    }
+    if (best_ns == 0 || best_warps <= 0) return cudaErrorInvalidConfiguration;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, best_smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.Rx_reg + Cfg::RC - 1) / Cfg::RC,
+              (kr1 - kr0 + Cfg::TRY * best_ns - 1) / (Cfg::TRY * best_ns), p.B);
+    kern<<<grid, 64 * best_ns, best_smem, stream>>>(p, best_ns);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D) \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D>>(const MatchParams&, cudaStream_t, int*);
+
+}  // namespace gbm3d

@@ -1,0 +1,201 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle, bit-exact on
+idx, dist and n_valid (integer work: every output is unique under the (d, idx) order,
+DESIGN.md reading R5, so array_equal is the bar)."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, config_images, special_image
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _gbm3d():
+    import paper_2103_10765_b200 as g
+    return g
+
+
+def _gpu(img, P, s, r, K, tau, method="auto"):
+    g = _gbm3d()
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    idx, dist, nv = g.block_match(t, P, s, r, K, tau, method=method)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), dist.cpu().numpy(), nv.cpu().numpy()
+
+
+def _assert_same(got, exp, what=""):
+    names = ("idx", "dist", "n_valid")
+    for g_, e_, n in zip(got, exp, names):
+        if not np.array_equal(g_, e_):
+            bad = np.argwhere(g_ != e_)
+            pytest.fail(f"{what} {n} differs at {len(bad)} positions, first {bad[:5].tolist()}: "
+                        f"got {g_[tuple(bad[0])]} expected {e_[tuple(bad[0])]}")
+
+
+# ----------------------------------------------------------------- the five BASELINE configs
+@pytest.mark.parametrize("name,ci", [("c0", 0), ("c1", 0), ("c1", 1), ("c2", 0)])
+def test_config_parity_small(name, ci):
+    cfg = CONFIGS[name]
+    c = cfg.calls[ci]
+    img = config_images(cfg)[0]
+    _assert_same(_gpu(img, c.patch, c.stride, c.radius, c.K, c.tau),
+                 oracle.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau), name)
+
+
+def test_config_parity_c3_full():
+    """2048^2, K=32: whole table bit-exact (the bench's launch configuration)."""
+    cfg = CONFIGS["c3"]
+    c = cfg.calls[0]
+    img = config_images(cfg)[0]
+    _assert_same(_gpu(img, c.patch, c.stride, c.radius, c.K, c.tau),
+                 oracle.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau), "c3")
+
+
+def test_config_parity_c4_all_images():
+    """Batch of 64 512^2 images in ONE batched launch (the bench's configuration)."""
+    cfg = CONFIGS["c4"]
+    c = cfg.calls[0]
+    imgs = config_images(cfg)
+    got = _gpu(imgs, c.patch, c.stride, c.radius, c.K, c.tau)
+    exp = oracle.block_match_batched(imgs, c.patch, c.stride, c.radius, c.K, c.tau)
+    _assert_same(got, exp, "c4")
+
+
+# ----------------------------------------------------------------- shapes and edge cases
+EDGE = [
+    # (H, W, P, s, r, K, tau, kind)
+    (8, 8, 8, 3, 19, 16, None, "uniform"),      # H = W = P: a single reference, window of one
+    (8, 40, 8, 3, 19, 16, None, "uniform"),     # H = P
+    (40, 8, 8, 3, 5, 16, None, "uniform"),      # W = P
+    (37, 53, 8, 3, 0, 16, None, "uniform"),     # r = 0
+    (30, 31, 8, 3, 32, 64, None, "uniform"),    # r >= H: global search, K > window count
+    (45, 61, 8, 3, 19, 1, None, "uniform"),     # K = 1
+    (45, 61, 8, 3, 19, 16, 0, "uniform"),       # tau = 0
+    (45, 61, 8, 3, 19, 16, 90000, "uniform"),   # tau active
+    (65, 33, 8, 3, 19, 32, None, "uniform"),    # odd W, ragged tiles
+    (70, 29, 8, 3, 7, 16, None, "uniform"),     # W < 32 reference columns
+    (200, 300, 8, 3, 19, 32, None, "uniform"),  # several CTAs x warps, ragged tail
+    (60, 70, 8, 9, 19, 16, None, "uniform"),    # stride > patch (direct kernel)
+    (60, 70, 8, 8, 19, 16, None, "uniform"),    # stride = patch (paper tiling, direct)
+    (61, 59, 12, 4, 19, 16, 720000, "uniform"),
+    (81, 97, 8, 2, 11, 16, None, "uniform"),
+    (81, 97, 8, 4, 19, 24, None, "uniform"),
+    (50, 50, 5, 2, 6, 10, None, "uniform"),     # no fast kernel: direct
+    (64, 64, 16, 16, 32, 64, None, "uniform"),  # maximum patch, radius, K
+    (70, 90, 8, 3, 19, 16, None, "constant"),   # all-zero distances: pure tie order
+    (70, 90, 8, 3, 19, 32, None, "periodic"),
+    (70, 90, 8, 3, 19, 16, None, "checker"),
+]
+
+
+@pytest.mark.parametrize("H,W,P,s,r,K,tau,kind", EDGE)
+def test_edge_cases(H, W, P, s, r, K, tau, kind):
+    img = special_image(kind, H, W, seed=H * 1000 + W, lo=-250, hi=500, value=77)
+    _assert_same(_gpu(img, P, s, r, K, tau), oracle.block_match(img, P, s, r, K, tau),
+                 f"{kind} {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz(seed):
+    rng = np.random.default_rng(100 + seed)
+    P, s = [(8, 3), (12, 4), (8, 2), (8, 4), (6, 3), (3, 1)][seed % 6]
+    H = int(rng.integers(P, 140))
+    W = int(rng.integers(P, 140))
+    r = int(rng.integers(0, 25))
+    K = int(rng.integers(1, 65))
+    tau = [None, int(rng.integers(0, 300000))][seed % 2]
+    img = special_image("uniform", H, W, seed=seed, lo=-200, hi=455)
+    _assert_same(_gpu(img, P, s, r, K, tau), oracle.block_match(img, P, s, r, K, tau),
+                 f"fuzz {seed}: {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
+
+
+def test_large_distances_exact_fallback():
+    """Distances above the 32-bit key's d range (2^21-1 at r=19) with no tau: lists fill
+    with saturated-range candidates and the in-kernel exact path must take over."""
+    img = special_image("uniform", 60, 70, seed=9, lo=-1400, hi=1400)  # E[d] ~ 8e7 >> 2^21
+    _assert_same(_gpu(img, 8, 3, 19, 16, None), oracle.block_match(img, 8, 3, 19, 16, None),
+                 "large distances")
+
+
+def test_int16_extremes_within_precondition():
+    rng = np.random.default_rng(3)
+    img = rng.choice(np.array([-2896, 2896, 0, 1000], np.int16), size=(50, 60))  # 8^2*5792^2 < 2^31
+    _assert_same(_gpu(img, 8, 3, 19, 16, None), oracle.block_match(img, 8, 3, 19, 16, None),
+                 "extremes")
+
+
+def test_direct_method_agrees():
+    img = config_images("c0")[0]
+    _assert_same(_gpu(img, 8, 3, 19, 16, None, method="direct"),
+                 oracle.block_match(img, 8, 3, 19, 16, None), "direct")
+
+
+# ----------------------------------------------------------------- variants (reading R16)
+def test_batched_equals_single_calls():
+    imgs = config_images("c4", n_images=3)[:, :200, :180].copy()
+    g = _gbm3d()
+    tb = torch.from_numpy(imgs).cuda()
+    bi, bd, bn = g.block_match(tb, 8, 3, 19, 16)
+    for i in range(3):
+        si, sd, sn = g.block_match(tb[i].contiguous(), 8, 3, 19, 16)
+        assert torch.equal(bi[i], si) and torch.equal(bd[i], sd) and torch.equal(bn[i], sn)
+
+
+@pytest.mark.parametrize("cuts", [[7, 30], [1, 2, 64, 65], [33], [65]])
+def test_row_ranges_concatenate_to_full(cuts):
+    """Emulated sharding on one GPU: slabs with halo rows, global indices."""
+    g = _gbm3d()
+    img = config_images("c1")[0][:201, :].copy()   # 201 x 256 -> Ry = 66 (appended last row)
+    H, W, P, s, r, K = 201, 256, 8, 3, 19, 32
+    Ry, Rx = g.grid_dims(H, W, P, s)
+    assert Ry == 66
+    splits = [0] + cuts + [Ry]
+    full = [t.cpu() for t in g.block_match(torch.from_numpy(img).cuda(), P, s, r, K)]
+    parts = []
+    for a, b in zip(splits[:-1], splits[1:]):
+        y0 = min(a * s, H - P)
+        y1 = min(b - 1, Ry - 1)
+        ylast = min(y1 * s, H - P)
+        lo, hi = max(0, y0 - r), min(H, ylast + r + P)
+        slab = torch.from_numpy(img[lo:hi].copy()).cuda()
+        parts.append([t.cpu() for t in g.block_match_rows(slab, lo, H, W, P, s, r, K, None, a, b)])
+    for i in range(3):
+        assert torch.equal(torch.cat([p[i] for p in parts]), full[i])
+
+
+def test_rows_rejects_short_slab():
+    g = _gbm3d()
+    img = torch.zeros((100, 64), dtype=torch.int16, device="cuda")
+    with pytest.raises(g.GBM3DError):
+        g.block_match_rows(img[10:50].contiguous(), 10, 200, 64, 8, 3, 19, 16, None, 10, 20)
+
+
+def test_host_entry_matches_device_entry():
+    g = _gbm3d()
+    imgs = config_images("c4", n_images=2)
+    h = torch.from_numpy(imgs).pin_memory()
+    hi, hd, hn = g.block_match_host(h, 8, 3, 19, 16)
+    di, dd, dn = g.block_match(torch.from_numpy(imgs).cuda(), 8, 3, 19, 16)
+    assert torch.equal(hi, di.cpu()) and torch.equal(hd, dd.cpu()) and torch.equal(hn, dn.cpu())
+
+
+def test_check_range_and_error_codes():
+    g = _gbm3d()
+    ok = torch.from_numpy(config_images("c0")[0]).cuda()
+    assert g.check_range(ok, 8)
+    bad = torch.tensor([[-20000, 20000], [0, 1]], dtype=torch.int16, device="cuda")
+    assert not g.check_range(bad, 2)
+    with pytest.raises(g.GBM3DError):
+        g.block_match(bad, 2, 1, 1, 2)            # check=True refuses out-of-domain images
+    with pytest.raises(g.GBM3DError):
+        g.block_match(ok, 17, 3, 19, 16)          # patch > 16 -> UNSUPPORTED
+
+
+def test_deterministic_repeat():
+    img = torch.from_numpy(config_images("c2")[0]).cuda()
+    g = _gbm3d()
+    a = g.block_match(img, 12, 4, 19, 16, 720000)
+    b = g.block_match(img, 12, 4, 19, 16, 720000)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)

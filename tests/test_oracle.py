@@ -346,3 +346,17 @@ def test_fft_cross_correlation_loose_check():
                 d = norms[ry, rx] + norms[cy, cx] - 2 * ip[cy, cx]
                 assert abs(d - dist[py, px, k]) < 1e-6 * max(1.0, abs(d)) + 1e-3
                 assert math.isclose(round(d), dist[py, px, k])
+
+
+def test_refs_entry_matches_whole_image():
+    """The per-reference entry (used for sampled full-size checks) equals the whole-image
+    routine cell by cell (both are the literal definition)."""
+    img = config_images("c1")[0][:100, :90]
+    idx, dist, nv = oracle.block_match(img, 8, 3, 19, 32, 25600 * 4)
+    rng = np.random.default_rng(1)
+    py = rng.integers(0, idx.shape[0], 50)
+    px = rng.integers(0, idx.shape[1], 50)
+    i2, d2, n2 = oracle.block_match_refs(img, 8, 3, 19, 32, 25600 * 4, py, px)
+    np.testing.assert_array_equal(i2, idx[py, px])
+    np.testing.assert_array_equal(d2, dist[py, px])
+    np.testing.assert_array_equal(n2, nv[py, px])
