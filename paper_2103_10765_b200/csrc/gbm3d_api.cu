@@ -16,22 +16,21 @@ static thread_local int g_last_launches = 0;
 // Fast-path table: (patch, stride) pairs with an instantiated strip kernel.
 static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok) {
     *ok = true;
+#define GBM3D_CASE(PP, SS, TRY, D)                                                             \
+    case PP * 100 + SS:                                                                        \
+        return p.cb == 11 ? launch_strip<StripCfg<PP, SS, TRY, D, 11>>(p, st, launches)       \
+                          : launch_strip<StripCfg<PP, SS, TRY, D, 13>>(p, st, launches);
     switch (p.P * 100 + p.S) {
-        case 803: return launch_strip<StripCfg<8, 3, 8, 5>>(p, st, launches);
-        case 1204: return launch_strip<StripCfg<12, 4, 4, 4>>(p, st, launches);
-        case 802: return launch_strip<StripCfg<8, 2, 8, 5>>(p, st, launches);
-        case 804: return launch_strip<StripCfg<8, 4, 6, 4>>(p, st, launches);
+        GBM3D_CASE(8, 3, 8, 5)
+        GBM3D_CASE(12, 4, 4, 4)
+        GBM3D_CASE(8, 2, 8, 5)
+        GBM3D_CASE(8, 4, 6, 4)
         default: *ok = false; return cudaSuccess;
     }
+#undef GBM3D_CASE
 }
 
 static int grid_count(int L, int P, int S) { return (L - P) / S + 1 + (((L - P) % S) ? 1 : 0); }
-
-static int ceil_log2(long long v) {
-    int b = 0;
-    while ((1LL << b) < v) ++b;
-    return b;
-}
 
 // Validate and fill the launch parameters shared by every entry point.
 static int make_params(MatchParams& p, int B, int H, int W, int patch, int stride, int radius,
@@ -61,7 +60,8 @@ static int make_params(MatchParams& p, int B, int H, int W, int patch, int strid
     p.row_begin = 0;
     p.row_end = p.Ry;
     p.side = 2 * radius + 1;
-    p.cb = ceil_log2((long long)p.side * p.side + 1);
+    // key = d << cb | code with 2^cb > side^2: cb = 11 for radius <= 22, 13 up to radius 32
+    p.cb = ((long long)p.side * p.side < 2048) ? 11 : 13;
     p.dsat = (uint32_t)((1ULL << (32 - p.cb)) - 1ULL);
     const int64_t taum1 = tau - 1;  // strict: d < tau  <=>  d <= tau - 1
     p.tdr0 = (int)(taum1 < (int64_t)p.dsat ? taum1 : (int64_t)p.dsat);

@@ -33,9 +33,10 @@ namespace gbm3d {
 
 constexpr int HEAP_STRIDE = 33;  // words per heap row: conflict-free per-lane AND per-ref access
 
-template <int P_, int S_, int TRY_, int D_>
+template <int P_, int S_, int TRY_, int D_, int CB_>
 struct StripCfg {
     static constexpr int P = P_, S = S_, TRY = TRY_, D = D_;
+    static constexpr int CB = CB_;  // key = d << CB | code; 2^CB > (2r+1)^2
     static constexpr int Q = P / S, REM = P % S;
     static constexpr int HL = (P + S - 1) / S - 1;       // helper lanes (no references)
     static constexpr int RC = 32 - HL;                   // reference columns per warp
@@ -44,7 +45,22 @@ struct StripCfg {
     static constexpr int COLS = 32 * S;                  // pixel columns covered by a warp
     static_assert(S <= P, "fast path needs stride <= patch");
     static_assert(TRY % 2 == 0, "the two warps of a strip split the reference rows");
+    static_assert(D <= 15, "queue lengths are packed in 4 bits");
 };
+
+// Heap capacity: the smallest perfect binary tree (2^h - 1 nodes) holding n keys.  The slots
+// beyond n hold 0-valued pads, which never rise above a real key, so the root stays the n-th
+// smallest key seen and the sift-down has a fixed depth h - 1.
+__host__ __device__ inline int heap_pad(int n) {
+    int c = 0;
+    while (c < n) c = 2 * c + 1;
+    return c;
+}
+__host__ __device__ inline int heap_levels(int npad) {  // sift levels = h - 1
+    int h = 0;
+    while ((1 << h) - 1 < npad) ++h;
+    return h > 0 ? h - 1 : 0;
+}
 
 // Shared-memory geometry of one CTA (host and device agree on it).
 struct StripSmem {
@@ -55,7 +71,7 @@ struct StripSmem {
         g.pitch = (COLS + 2 * r + 1) & ~1;
         g.rows = S * (TRY * NS - 1) + P + 2 * r + (D - 1);  // + D-1 rows read by the dy tail block
         g.img_bytes = ((g.rows * g.pitch * 2) + 15) & ~15;
-        g.heap_words = NS * TRY * (K - 1) * HEAP_STRIDE;
+        g.heap_words = NS * TRY * heap_pad(K - 1) * HEAP_STRIDE;
         g.queue_words = 2 * NS * TRY * D * 32;
         g.count_bytes = 2 * NS * TRY * 32;
         return g;
@@ -65,21 +81,26 @@ struct StripSmem {
     }
 };
 
-// Max-heap of n keys at H[i * HEAP_STRIDE]: replace the root by key (key < root) and sift down.
-static __device__ __forceinline__ void heap_replace_root(uint32_t* H, int n, uint32_t key) {
-    int i = 0;
-    for (;;) {
-        const int c = 2 * i + 1;
-        if (c >= n) break;
-        const uint32_t v1 = H[c * HEAP_STRIDE];
-        const uint32_t v2 = (c + 1 < n) ? H[(c + 1) * HEAP_STRIDE] : 0u;
-        const bool right = v2 > v1;
-        const uint32_t big = right ? v2 : v1;
-        if (big < key) break;  // keys are unique
-        H[i * HEAP_STRIDE] = big;
-        i = right ? c + 1 : c;
+// Max-heap (perfect tree, `levels` = h - 1) of one reference: slot i at byte offset i * ROWB
+// from Hb.  Replace the root by key (key < root) and sift down, branch-free, fixed depth.
+constexpr int HEAP_ROWB = HEAP_STRIDE * 4;
+static __device__ __forceinline__ void heap_replace_root(char* Hb, int levels, uint32_t key) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int lv = 0; lv < 6; ++lv) {
+        if (lv < levels) {
+            const uint32_t oc = 2 * o + HEAP_ROWB;  // left child of slot o / ROWB
+            const uint32_t v1 = *reinterpret_cast<const uint32_t*>(Hb + oc);
+            const uint32_t v2 = *reinterpret_cast<const uint32_t*>(Hb + oc + HEAP_ROWB);
+            const bool right = v2 > v1;
+            const uint32_t big = right ? v2 : v1;
+            const bool go = big > key;
+            *reinterpret_cast<uint32_t*>(Hb + o) = go ? big : key;
+            const uint32_t on = right ? oc + HEAP_ROWB : oc;
+            o = go ? on : o;
+        }
     }
-    H[i * HEAP_STRIDE] = key;
+    *reinterpret_cast<uint32_t*>(Hb + o) = key;
 }
 
 // In-place heapsort of a max-heap of n keys -> ascending order.
@@ -104,17 +125,29 @@ static __device__ void heap_sort(uint32_t* H, int n) {
     }
 }
 
+// i-th element of the centre-out sequence c, c+1, c-1, c+2, c-2, ... over [0, n).
+static __device__ __forceinline__ int center_out(int i, int c, int n) {
+    if (i == 0) return c;
+    const int lo = c, hi = n - 1 - c, m = min(lo, hi);
+    if (i <= 2 * m) {
+        const int s = (i + 1) >> 1;
+        return (i & 1) ? c + s : c - s;
+    }
+    const int extra = i - 2 * m;
+    return hi > lo ? c + m + extra : c - m - extra;
+}
+
 static __device__ __forceinline__ void pair_sync(int strip) {
     asm volatile("bar.sync %0, 64;" ::"r"(strip + 1) : "memory");
 }
 
 // One displacement block: D consecutive dy at a fixed dx, all TRY reference rows of the lane.
-template <class Cfg, bool MASKED>
+template <class Cfg>
 __device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, int pitch, int brow,
                                             int bcol, const int (&a)[Cfg::NR][Cfg::S],
                                             const int (&tdr)[Cfg::TRY], uint32_t* (&qp)[Cfg::TRY],
                                             const uint32_t (&mk)[Cfg::TRY], uint32_t code0,
-                                            uint32_t side, uint32_t mulcb) {
+                                            uint32_t side) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
     constexpr int Q = Cfg::Q, REM = Cfg::REM, NCH = Cfg::NCH;
     int Cc[D][NCH][S];
@@ -156,10 +189,10 @@ __device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, 
 #pragma unroll
                 for (int q = 1; q < Q; ++q) d += __shfl_down_sync(0xffffffffu, hc, q);
                 if (REM > 0) d += __shfl_down_sync(0xffffffffu, ha, Q);
-                bool pass = d <= tdr[k];
-                if (MASKED) pass = pass && ((mk[k] >> j) & 1u);
+                // gate: one compare with the heap-root copy, AND the border/self mask bit
+                const bool pass = (d <= tdr[k]) && ((mk[k] >> j) & 1u);
                 if (pass) {
-                    *qp[k] = (uint32_t)d * mulcb + (code0 + (uint32_t)j * side);
+                    *qp[k] = ((uint32_t)d << Cfg::CB) + (code0 + (uint32_t)j * side);
                     qp[k] += 32;
                 }
             }
@@ -171,13 +204,13 @@ __device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, 
 // key range may have dropped a valid candidate (tau - 1 > dsat and the heap is not full).
 // The list lives directly in the output slots 1..K-1.  Returns the number of matches.
 static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ sm_img, int pitch,
-                                                   int sy, int sx, int ry, int rx,
-                                                   const MatchParams& p, int32_t* oi,
+                                                   int sy, int sx, int ry, int rx, int H, int W,
+                                                   int P, int r, int K, int64_t tau, int32_t* oi,
                                                    int32_t* od) {
-    const int L = p.K - 1, P = p.P, r = p.r;
+    const int L = K - 1;
     int cnt = 0;
-    const int cy0 = max(0, ry - r), cy1 = min(p.H - P, ry + r);
-    const int cx0 = max(0, rx - r), cx1 = min(p.W - P, rx + r);
+    const int cy0 = max(0, ry - r), cy1 = min(H - P, ry + r);
+    const int cx0 = max(0, rx - r), cx1 = min(W - P, rx + r);
     for (int cy = cy0; cy <= cy1; ++cy) {
         for (int cx = cx0; cx <= cx1; ++cx) {
             if (cy == ry && cx == rx) continue;
@@ -190,8 +223,8 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
                     d += df * df;
                 }
             }
-            if (d >= p.tau) continue;
-            const uint64_t key = ((uint64_t)d << 32) | (uint32_t)(cy * p.W + cx);
+            if (d >= tau) continue;
+            const uint64_t key = ((uint64_t)d << 32) | (uint32_t)(cy * W + cx);
             int pos;
             if (cnt < L) {
                 pos = cnt++;
@@ -208,10 +241,10 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
                 --pos;
             }
             od[pos + 1] = (int32_t)d;
-            oi[pos + 1] = cy * p.W + cx;
+            oi[pos + 1] = cy * W + cx;
         }
     }
-    const int self = ry * p.W + rx;
+    const int self = ry * W + rx;
     oi[0] = self;
     od[0] = 0;
     for (int i = cnt; i < L; ++i) {
@@ -224,10 +257,12 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
 template <class Cfg>
 __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
-    constexpr int RC = Cfg::RC;
+    constexpr int RC = Cfg::RC, CB = Cfg::CB, HALF = TRY / 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int r = p.r;
     const int L = p.K - 1;
+    const int LP = heap_pad(L);          // heap slots (perfect tree)
+    const int LV = heap_levels(LP);      // sift levels
     const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K);
     int16_t* sm_img = reinterpret_cast<int16_t*>(smem_raw);
     uint32_t* sm_heap = reinterpret_cast<uint32_t*>(smem_raw + g.img_bytes);
@@ -242,7 +277,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     const int m0 = (int)blockIdx.x * RC;
     const int16_t* __restrict__ img = p.img + (int64_t)b * p.img_bstride;
 
-    // ---- stage tile + halo (int16, zero outside the image / slab) and reset the heaps
+    // ---- stage tile + halo (int16, zero outside the image / slab); heaps: INF keys, 0 pads
     {
         const int gy0 = S * k0 - r, gx0 = S * m0 - r;
         const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
@@ -255,7 +290,10 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                 sm_img[yy * g.pitch + xx] = (rowok && gx >= 0 && gx < p.W) ? src[gx] : (int16_t)0;
             }
         }
-        for (int i = threadIdx.x; i < g.heap_words; i += blockDim.x) sm_heap[i] = KEY_INF;
+        for (int i = threadIdx.x; i < g.heap_words; i += blockDim.x) {
+            const int slot = (i / HEAP_STRIDE) % (LP > 0 ? LP : 1);
+            sm_heap[i] = slot < L ? KEY_INF : 0u;
+        }
     }
     __syncthreads();
 
@@ -273,9 +311,9 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
 #pragma unroll
         for (int c = 0; c < S; ++c) a[y][c] = sm_img[(arow0 + y) * g.pitch + r + S * lane + c];
 
-    uint32_t* const heap0 = sm_heap + (strip * TRY) * L * HEAP_STRIDE + lane;  // + k*L*33
-    uint32_t* const qw = sm_q + (warp * TRY * D) * 32 + lane;                 // own queues
-    uint32_t* const qo = sm_q + ((warp ^ 1) * TRY * D) * 32 + lane;           // partner's
+    uint32_t* const heap0 = sm_heap + (strip * TRY) * LP * HEAP_STRIDE + lane;  // + k*LP*33
+    uint32_t* const qw = sm_q + (warp * TRY * D) * 32 + lane;                  // own queues
+    uint32_t* const qo = sm_q + ((warp ^ 1) * TRY * D) * 32 + lane;            // partner's
     uint8_t* const cw = sm_cnt + (warp * TRY) * 32 + lane;
     uint8_t* const co = sm_cnt + ((warp ^ 1) * TRY) * 32 + lane;
 
@@ -291,7 +329,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     const int ry_first = S * kw, ry_last = S * (kw + nk - 1);
     const int rx_first = S * m0, rx_last = S * (m0 + nm - 1);
     const int ylast = p.H - P, xlast = p.W - P;
-    const uint32_t side = (uint32_t)p.side, mulcb = 1u << p.cb;
+    const uint32_t side = (uint32_t)p.side;
     const int nDY = (p.side + D - 1) / D;
     const int NB = p.side * nDY;  // displacement blocks (dx-major)
 
@@ -299,23 +337,22 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
         for (int it = 0; it < NB; it += 2) {
             const int blk = it + half;
             if (blk < NB) {
-                const int dx = -r + blk / nDY;
-                const int dy0 = -r + (blk % nDY) * D;
-                const bool xvalid = (S * m + dx >= 0) && (S * m + dx <= xlast);
-                const bool colx_ok = (rx_first + dx >= 0) && (rx_last + dx <= xlast);
+                // centre-out visiting order (dx: 0, +1, -1, +2, ...; dy blocks likewise): the
+                // nearest displacements usually match best, so the heap gates tighten early
+                const int dx = center_out(blk / nDY, r, 2 * r + 1) - r;
+                const int dy0 = -r + center_out(blk % nDY, r / D, nDY) * D;
                 const int bcol = r + S * lane + dx;
                 const int brow = arow0 + dy0;
                 const uint32_t code0 = (uint32_t)((dy0 + r) * p.side + (dx + r));
-                const bool unmasked = colx_ok && (ry_first + dy0 >= 0) &&
-                                      (ry_last + dy0 + D - 1 <= ylast) && (dy0 + D - 1 <= r) &&
-                                      !(dx == 0 && dy0 <= 0 && dy0 + D > 0);
+                const bool interior = (rx_first + dx >= 0) && (rx_last + dx <= xlast) &&
+                                      (ry_first + dy0 >= 0) && (ry_last + dy0 + D - 1 <= ylast) &&
+                                      (dy0 + D - 1 <= r) && !(dx == 0 && dy0 <= 0 && dy0 + D > 0);
                 uint32_t mk[TRY];
-                if (unmasked) {
+                if (interior) {
 #pragma unroll
                     for (int k = 0; k < TRY; ++k) mk[k] = 0xffffffffu;
-                    strip_block<Cfg, false>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0,
-                                            side, mulcb);
-                } else {
+                } else {  // border / window-tail / self: per (row, dy) validity bits
+                    const bool xvalid = (S * m + dx >= 0) && (S * m + dx <= xlast);
                     uint32_t jx = 0;
 #pragma unroll
                     for (int j = 0; j < D; ++j) {
@@ -331,30 +368,58 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                             hi >= lo ? (((2u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
                         mk[k] = jx & ym;
                     }
-                    strip_block<Cfg, true>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0,
-                                           side, mulcb);
                 }
+                strip_block<Cfg>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0, side);
             }
-            // publish queue lengths, then merge: this warp owns reference rows k = half (mod 2)
+            // publish queue lengths; this warp merges reference rows k = half (mod 2)
 #pragma unroll
             for (int k = 0; k < TRY; ++k) {
                 cw[k * 32] = (uint8_t)((qp[k] - (qw + k * D * 32)) >> 5);
                 qp[k] = qw + k * D * 32;
             }
             pair_sync(strip);
+            {
+                // flattened per-thread task loop over groups g = 2*kk + src.  Thread (half, lane)
+                // merges rows k = half + 2 kk, each in column (lane + 5 k) mod 32: spreading a
+                // thread's heaps over distant columns decorrelates their task counts.
+                uint32_t packed = 0, nonempty = 0;
+                int T = 0;
 #pragma unroll
-            for (int k = half; k < TRY; k += 2) {
-                uint32_t* const H = heap0 + k * L * HEAP_STRIDE;
-                uint32_t thr = min(H[0], p.thr0);
-#pragma unroll
-                for (int src = 0; src < 2; ++src) {
-                    const uint32_t* qk = (src ? qo : qw) + k * D * 32;
-                    const int n = (src ? co : cw)[k * 32];
-                    for (int i = 0; i < n; ++i) {
-                        const uint32_t key = qk[i * 32];
+                for (int kk = 0; kk < HALF; ++kk) {
+                    const int k = half + 2 * kk;
+                    const int col = (lane + 5 * k) & 31;
+                    const uint32_t n0 = sm_cnt[(warp * TRY + k) * 32 + col];
+                    const uint32_t n1 = sm_cnt[((warp ^ 1) * TRY + k) * 32 + col];
+                    packed |= (n0 << (8 * kk)) | (n1 << (8 * kk + 4));
+                    nonempty |= ((n0 ? 1u : 0u) << (2 * kk)) | ((n1 ? 1u : 0u) << (2 * kk + 1));
+                    T += (int)(n0 + n1);
+                }
+                if (T > 0) {
+                    char* const heapb = reinterpret_cast<char*>(sm_heap + (strip * TRY) * LP * HEAP_STRIDE);
+                    int gq = __ffs(nonempty) - 1;
+                    int n = (packed >> (4 * gq)) & 15u, i = 0;
+                    int k = half + 2 * (gq >> 1), col = (lane + 5 * k) & 31;
+                    char* Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
+                    const uint32_t* q = sm_q + (((warp ^ (gq & 1)) * TRY + k) * D) * 32 + col;
+                    uint32_t thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
+                    for (int t = 0; t < T; ++t) {
+                        const uint32_t key = q[i * 32];
                         if (key < thr) {
-                            heap_replace_root(H, L, key);
-                            thr = min(H[0], p.thr0);
+                            heap_replace_root(Hb, LV, key);
+                            thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
+                        }
+                        if (++i == n) {
+                            nonempty &= ~(1u << gq);
+                            if (nonempty) {
+                                gq = __ffs(nonempty) - 1;
+                                n = (packed >> (4 * gq)) & 15u;
+                                i = 0;
+                                k = half + 2 * (gq >> 1);
+                                col = (lane + 5 * k) & 31;
+                                Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
+                                q = sm_q + (((warp ^ (gq & 1)) * TRY + k) * D) * 32 + col;
+                                thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
+                            }
                         }
                     }
                 }
@@ -363,24 +428,25 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
 #pragma unroll
             for (int k = 0; k < TRY; ++k) {
                 if (refok[k]) {
-                    const uint32_t thr = min(heap0[k * L * HEAP_STRIDE], p.thr0);
-                    tdr[k] = thr == p.thr0 ? p.tdr0 : (int)(thr >> p.cb);
+                    const uint32_t thr = min(heap0[k * LP * HEAP_STRIDE], p.thr0);
+                    tdr[k] = thr == p.thr0 ? p.tdr0 : (int)(thr >> CB);
                 }
             }
         }
         // ---- order each heap ascending (in place), each warp its own reference rows
 #pragma unroll 1
         for (int k = half; k < TRY; k += 2)
-            if (refok[k]) heap_sort(heap0 + k * L * HEAP_STRIDE, L);
+            if (refok[k]) heap_sort(heap0 + k * LP * HEAP_STRIDE, LP);
         pair_sync(strip);
     }
 
     // ---- epilogue: coalesced rows; slot 0 = self (d = 0), ranks 1.. sorted keys, pads (self,-1)
-    const uint32_t cmask = (1u << p.cb) - 1u;
+    const uint32_t cmask = (1u << CB) - 1u;
+    const int off = LP - L;  // sorted heap: LP - L zero pads first, then the L keys ascending
 #pragma unroll 1
     for (int k = half; k < nk; k += 2) {
         const int kk = kw + k, ry = S * kk;
-        const uint32_t* Hk = sm_heap + (strip * TRY + k) * L * HEAP_STRIDE;
+        const uint32_t* Hk = sm_heap + (strip * TRY + k) * LP * HEAP_STRIDE;
 #pragma unroll 1
         for (int l = 0; l < nm; ++l) {
             const int rx = S * (m0 + l);
@@ -393,14 +459,14 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
             for (int s0 = 0; s0 < p.K; s0 += 32) {
                 const int s = s0 + lane;
                 uint32_t key = KEY_INF;
-                if (s >= 1 && s < p.K) key = Hk[(s - 1) * HEAP_STRIDE + l];
+                if (s >= 1 && s < p.K) key = Hk[(off + s - 1) * HEAP_STRIDE + l];
                 cnt += __popc(__ballot_sync(0xffffffffu, key != KEY_INF));
                 if (s < p.K) {
                     int32_t vi = self, vd = (s == 0) ? 0 : -1;
                     if (key != KEY_INF) {
                         const uint32_t code = key & cmask;
                         vi = (ry + (int)(code / side) - r) * p.W + rx + (int)(code % side) - r;
-                        vd = (int32_t)(key >> p.cb);
+                        vd = (int32_t)(key >> CB);
                     }
                     oi[s] = vi;
                     od[s] = vd;
@@ -412,8 +478,8 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                 if (cnt < wy * wx - 1) {
                     __syncwarp();
                     if (lane == 0)
-                        cnt = strip_exact_ref(sm_img, g.pitch, arow0 + S * k, r + S * l, ry, rx, p,
-                                              oi, od);
+                        cnt = strip_exact_ref(sm_img, g.pitch, arow0 + S * k, r + S * l, ry, rx,
+                                              p.H, p.W, P, r, p.K, p.tau, oi, od);
                     cnt = __shfl_sync(0xffffffffu, cnt, 0);
                 }
             }
@@ -460,7 +526,10 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     return cudaGetLastError();
 }
 
-#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D) \
-    template cudaError_t launch_strip<StripCfg<P, S, TRY, D>>(const MatchParams&, cudaStream_t, int*);
+#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D)                                                  \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 11>>(const MatchParams&,       \
+                                                                 cudaStream_t, int*);       \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 13>>(const MatchParams&,       \
+                                                                 cudaStream_t, int*);
 
 }  // namespace gbm3d

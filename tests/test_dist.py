@@ -1,0 +1,92 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sharding logic of
+paper_2103_10765_b200/dist.py: partitions, slab halos, and the point-to-point gather of row
+blocks into rank 0's full tables.  The CUDA kernels are exercised by the GPU tests
+(tests/test_gpu_parity.py::test_row_ranges_concatenate_to_full emulates the shards on one GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2103_10765_b200 import dist as gd
+
+
+def test_row_partition_covers_and_balances():
+    for Ry in (1, 7, 64, 681):
+        for world in (1, 2, 3, 4, 8):
+            parts = gd.row_partition(Ry, world)
+            assert parts[0][0] == 0 and parts[-1][1] == Ry
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def test_slab_bounds_contain_every_window():
+    """Every candidate row of every reference in [k0, k1) lies in the slab (clamped window)."""
+    for H, P, S, r in [(2048, 8, 3, 19), (201, 8, 3, 19), (512, 12, 4, 19), (50, 8, 3, 40)]:
+        Ry = gd.grid_counts(H, P, S)[1]
+        for world in (2, 4, 8):
+            for k0, k1 in gd.row_partition(Ry, world):
+                if k1 <= k0:
+                    continue
+                y0, y1 = gd.slab_bounds(H, P, S, r, k0, k1)
+                for k in range(k0, k1):
+                    ry = gd.ref_row_y(k, H, P, S)
+                    lo, hi = max(0, ry - r), min(H - P, ry + r) + P
+                    assert y0 <= lo and hi <= y1
+    # at 8 GPUs the c3 slabs are at most ~300 rows
+    Ry = gd.grid_counts(2048, 8, 3)[1]
+    assert max(np.diff(gd.slab_bounds(2048, 8, 3, 19, a, b))[0]
+               for a, b in gd.row_partition(Ry, 8)) <= 300
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Ry, Rx, K = 23, 5, 4
+        ranges = gd.row_partition(Ry, world)
+        a, b = ranges[rank]
+        # a fake table whose values encode the global row: what rank 0 must reassemble
+        idx = (torch.arange(a, b).view(-1, 1, 1) * 1000 + torch.arange(Rx * K).view(1, Rx, K)).int()
+        dst = -idx
+        nv = torch.arange(a, b).view(-1, 1).expand(-1, Rx).contiguous().int()
+        full = None
+        if rank == 0:
+            full = (torch.zeros((Ry, Rx, K), dtype=torch.int32),
+                    torch.zeros((Ry, Rx, K), dtype=torch.int32),
+                    torch.zeros((Ry, Rx), dtype=torch.int32))
+        gd.gather_rows((idx, dst, nv), full, ranges, rank, world)
+        if rank == 0:
+            exp = (torch.arange(Ry).view(-1, 1, 1) * 1000 + torch.arange(Rx * K).view(1, Rx, K)).int()
+            ok = (torch.equal(full[0], exp) and torch.equal(full[1], -exp)
+                  and torch.equal(full[2], torch.arange(Ry).view(-1, 1).expand(-1, Rx).int()))
+            q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gather_rows_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
