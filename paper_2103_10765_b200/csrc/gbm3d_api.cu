@@ -20,6 +20,13 @@ static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* la
     case PP * 100 + SS:                                                                        \
         return p.cb == 11 ? launch_strip<StripCfg<PP, SS, TRY, D, 11>>(p, st, launches)       \
                           : launch_strip<StripCfg<PP, SS, TRY, D, 13>>(p, st, launches);
+    static const bool solo = [] {
+        const char* v = getenv("GBM3D_STRIP_SOLO");  // tuning knob (experiments only)
+        return v && v[0] == '1';
+    }();
+    if (solo && p.P == 8 && p.S == 3)
+        return p.cb == 11 ? launch_strip<StripCfg<8, 3, 4, 8, 11, 1>>(p, st, launches)
+                          : launch_strip<StripCfg<8, 3, 4, 8, 13, 1>>(p, st, launches);
     switch (p.P * 100 + p.S) {
         GBM3D_CASE(8, 3, 8, 5)
         GBM3D_CASE(12, 4, 4, 4)

@@ -33,9 +33,10 @@ namespace gbm3d {
 
 constexpr int HEAP_STRIDE = 33;  // words per heap row: conflict-free per-lane AND per-ref access
 
-template <int P_, int S_, int TRY_, int D_, int CB_>
+template <int P_, int S_, int TRY_, int D_, int CB_, int WPS_ = 2>
 struct StripCfg {
     static constexpr int P = P_, S = S_, TRY = TRY_, D = D_;
+    static constexpr int WPS = WPS_;  // warps per strip: 2 = paired (shared heaps), 1 = solo
     static constexpr int CB = CB_;  // key = d << CB | code; 2^CB > (2r+1)^2
     static constexpr int Q = P / S, REM = P % S;
     static constexpr int HL = (P + S - 1) / S - 1;       // helper lanes (no references)
@@ -44,7 +45,8 @@ struct StripCfg {
     static constexpr int NCH = TRY - 1 + Q + (REM > 0);  // row chunks of a strip
     static constexpr int COLS = 32 * S;                  // pixel columns covered by a warp
     static_assert(S <= P, "fast path needs stride <= patch");
-    static_assert(TRY % 2 == 0, "the two warps of a strip split the reference rows");
+    static_assert(WPS == 1 || WPS == 2, "one or two warps per strip");
+    static_assert(TRY % WPS == 0, "the warps of a strip split the reference rows");
     static_assert(D <= 15, "queue lengths are packed in 4 bits");
 };
 
@@ -66,14 +68,14 @@ __host__ __device__ inline int heap_levels(int npad) {  // sift levels = h - 1
 struct StripSmem {
     int pitch, rows, img_bytes, heap_words, queue_words, count_bytes;
     __host__ __device__ static StripSmem make(int COLS, int S, int P, int TRY, int D, int NS, int r,
-                                              int K) {
+                                              int K, int WPS) {
         StripSmem g;
         g.pitch = (COLS + 2 * r + 1) & ~1;
         g.rows = S * (TRY * NS - 1) + P + 2 * r + (D - 1);  // + D-1 rows read by the dy tail block
         g.img_bytes = ((g.rows * g.pitch * 2) + 15) & ~15;
         g.heap_words = NS * TRY * heap_pad(K - 1) * HEAP_STRIDE;
-        g.queue_words = 2 * NS * TRY * D * 32;
-        g.count_bytes = 2 * NS * TRY * 32;
+        g.queue_words = WPS * NS * TRY * D * 32;
+        g.count_bytes = WPS * NS * TRY * 32;
         return g;
     }
     __host__ __device__ int bytes() const {
@@ -257,20 +259,20 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
 template <class Cfg>
 __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
-    constexpr int RC = Cfg::RC, CB = Cfg::CB, HALF = TRY / 2;
+    constexpr int RC = Cfg::RC, CB = Cfg::CB, WPS = Cfg::WPS, HALF = TRY / WPS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int r = p.r;
     const int L = p.K - 1;
     const int LP = heap_pad(L);          // heap slots (perfect tree)
     const int LV = heap_levels(LP);      // sift levels
-    const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K);
+    const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K, WPS);
     int16_t* sm_img = reinterpret_cast<int16_t*>(smem_raw);
     uint32_t* sm_heap = reinterpret_cast<uint32_t*>(smem_raw + g.img_bytes);
     uint32_t* sm_q = sm_heap + g.heap_words;
     uint8_t* sm_cnt = reinterpret_cast<uint8_t*>(sm_q + g.queue_words);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int strip = warp >> 1, half = warp & 1;
+    const int strip = warp / WPS, half = warp % WPS;
     const int b = blockIdx.z;
     const int kr0 = p.row_begin, kr1 = min(p.row_end, p.Ry_reg);  // regular rows in this call
     const int k0 = kr0 + (int)blockIdx.y * TRY * NS;
@@ -313,9 +315,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
 
     uint32_t* const heap0 = sm_heap + (strip * TRY) * LP * HEAP_STRIDE + lane;  // + k*LP*33
     uint32_t* const qw = sm_q + (warp * TRY * D) * 32 + lane;                  // own queues
-    uint32_t* const qo = sm_q + ((warp ^ 1) * TRY * D) * 32 + lane;            // partner's
     uint8_t* const cw = sm_cnt + (warp * TRY) * 32 + lane;
-    uint8_t* const co = sm_cnt + ((warp ^ 1) * TRY) * 32 + lane;
 
     int tdr[TRY];
     bool refok[TRY];
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     const int NB = p.side * nDY;  // displacement blocks (dx-major)
 
     if (L > 0) {
-        for (int it = 0; it < NB; it += 2) {
+        for (int it = 0; it < NB; it += WPS) {
             const int blk = it + half;
             if (blk < NB) {
                 // centre-out visiting order (dx: 0, +1, -1, +2, ...; dy blocks likewise): the
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                 cw[k * 32] = (uint8_t)((qp[k] - (qw + k * D * 32)) >> 5);
                 qp[k] = qw + k * D * 32;
             }
-            pair_sync(strip);
+            if (WPS == 2) pair_sync(strip); else __syncwarp();
             {
                 // flattened per-thread task loop over groups g = 2*kk + src.  Thread (half, lane)
                 // merges rows k = half + 2 kk, each in column (lane + 5 k) mod 32: spreading a
@@ -386,21 +386,23 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                 int T = 0;
 #pragma unroll
                 for (int kk = 0; kk < HALF; ++kk) {
-                    const int k = half + 2 * kk;
+                    const int k = half + WPS * kk;
                     const int col = (lane + 5 * k) & 31;
-                    const uint32_t n0 = sm_cnt[(warp * TRY + k) * 32 + col];
-                    const uint32_t n1 = sm_cnt[((warp ^ 1) * TRY + k) * 32 + col];
-                    packed |= (n0 << (8 * kk)) | (n1 << (8 * kk + 4));
-                    nonempty |= ((n0 ? 1u : 0u) << (2 * kk)) | ((n1 ? 1u : 0u) << (2 * kk + 1));
-                    T += (int)(n0 + n1);
+#pragma unroll
+                    for (int src = 0; src < WPS; ++src) {
+                        const uint32_t n = sm_cnt[((warp ^ src) * TRY + k) * 32 + col];
+                        packed |= n << (4 * (WPS * kk + src));
+                        nonempty |= (n ? 1u : 0u) << (WPS * kk + src);
+                        T += (int)n;
+                    }
                 }
                 if (T > 0) {
                     char* const heapb = reinterpret_cast<char*>(sm_heap + (strip * TRY) * LP * HEAP_STRIDE);
                     int gq = __ffs(nonempty) - 1;
                     int n = (packed >> (4 * gq)) & 15u, i = 0;
-                    int k = half + 2 * (gq >> 1), col = (lane + 5 * k) & 31;
+                    int k = half + WPS * (gq / WPS), col = (lane + 5 * k) & 31;
                     char* Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
-                    const uint32_t* q = sm_q + (((warp ^ (gq & 1)) * TRY + k) * D) * 32 + col;
+                    const uint32_t* q = sm_q + (((warp ^ (gq % WPS)) * TRY + k) * D) * 32 + col;
                     uint32_t thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
                     for (int t = 0; t < T; ++t) {
                         const uint32_t key = q[i * 32];
@@ -414,17 +416,17 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                                 gq = __ffs(nonempty) - 1;
                                 n = (packed >> (4 * gq)) & 15u;
                                 i = 0;
-                                k = half + 2 * (gq >> 1);
+                                k = half + WPS * (gq / WPS);
                                 col = (lane + 5 * k) & 31;
                                 Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
-                                q = sm_q + (((warp ^ (gq & 1)) * TRY + k) * D) * 32 + col;
+                                q = sm_q + (((warp ^ (gq % WPS)) * TRY + k) * D) * 32 + col;
                                 thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
                             }
                         }
                     }
                 }
             }
-            pair_sync(strip);
+            if (WPS == 2) pair_sync(strip); else __syncwarp();
 #pragma unroll
             for (int k = 0; k < TRY; ++k) {
                 if (refok[k]) {
@@ -435,16 +437,16 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
         }
         // ---- order each heap ascending (in place), each warp its own reference rows
 #pragma unroll 1
-        for (int k = half; k < TRY; k += 2)
+        for (int k = half; k < TRY; k += WPS)
             if (refok[k]) heap_sort(heap0 + k * LP * HEAP_STRIDE, LP);
-        pair_sync(strip);
+        if (WPS == 2) pair_sync(strip); else __syncwarp();
     }
 
     // ---- epilogue: coalesced rows; slot 0 = self (d = 0), ranks 1.. sorted keys, pads (self,-1)
     const uint32_t cmask = (1u << CB) - 1u;
     const int off = LP - L;  // sorted heap: LP - L zero pads first, then the L keys ascending
 #pragma unroll 1
-    for (int k = half; k < nk; k += 2) {
+    for (int k = half; k < nk; k += WPS) {
         const int kk = kw + k, ry = S * kk;
         const uint32_t* Hk = sm_heap + (strip * TRY + k) * LP * HEAP_STRIDE;
 #pragma unroll 1
@@ -501,17 +503,17 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     if (e != cudaSuccess) return e;
     auto kern = match_strip_kernel<Cfg>;
     int best_ns = 0, best_warps = -1, best_smem = 0;
-    for (int ns : {2, 1}) {
-        const int smem =
-            StripSmem::make(Cfg::COLS, Cfg::S, Cfg::P, Cfg::TRY, Cfg::D, ns, p.r, p.K).bytes();
+    for (int ns : {4 / Cfg::WPS, 2 / Cfg::WPS, 1}) {
+        const int smem = StripSmem::make(Cfg::COLS, Cfg::S, Cfg::P, Cfg::TRY, Cfg::D, ns, p.r, p.K,
+                                         Cfg::WPS).bytes();
         if (smem > max_optin) continue;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 64 * ns, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * Cfg::WPS * ns, smem);
         if (e != cudaSuccess) return e;
-        if (nb * 2 * ns > best_warps) {
-            best_warps = nb * 2 * ns;
+        if (nb * Cfg::WPS * ns > best_warps) {
+            best_warps = nb * Cfg::WPS * ns;
             best_ns = ns;
             best_smem = smem;
         }
@@ -521,15 +523,15 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     if (e != cudaSuccess) return e;
     dim3 grid((p.Rx_reg + Cfg::RC - 1) / Cfg::RC,
               (kr1 - kr0 + Cfg::TRY * best_ns - 1) / (Cfg::TRY * best_ns), p.B);
-    kern<<<grid, 64 * best_ns, best_smem, stream>>>(p, best_ns);
+    kern<<<grid, 32 * Cfg::WPS * best_ns, best_smem, stream>>>(p, best_ns);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
 
-#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D)                                                  \
-    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 11>>(const MatchParams&,       \
-                                                                 cudaStream_t, int*);       \
-    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 13>>(const MatchParams&,       \
-                                                                 cudaStream_t, int*);
+#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D, WPS)                                             \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 11, WPS>>(const MatchParams&,  \
+                                                                      cudaStream_t, int*);  \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 13, WPS>>(const MatchParams&,  \
+                                                                      cudaStream_t, int*);
 
 }  // namespace gbm3d
