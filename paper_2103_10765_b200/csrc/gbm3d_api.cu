@@ -13,28 +13,30 @@ namespace gbm3d {
 
 static thread_local int g_last_launches = 0;
 
-// Fast-path table: (patch, stride) pairs with an instantiated strip kernel.
+// Fast-path table: (patch, stride) pairs with an instantiated strip kernel.  Heap depth by K
+// (15 / 31 / 63 slots), key shift CB by radius (11 for r <= 22, 13 up to 32).
+template <int PP, int SS, int TRY, int D, int WPS>
+static cudaError_t launch_shape(const MatchParams& p, cudaStream_t st, int* launches) {
+    const int L = p.K - 1;
+    if (p.cb == 11) {
+        if (L <= 15) return launch_strip<StripCfg<PP, SS, TRY, D, 11, WPS, 3>>(p, st, launches);
+        if (L <= 31) return launch_strip<StripCfg<PP, SS, TRY, D, 11, WPS, 4>>(p, st, launches);
+        return launch_strip<StripCfg<PP, SS, TRY, D, 11, WPS, 5>>(p, st, launches);
+    }
+    if (L <= 15) return launch_strip<StripCfg<PP, SS, TRY, D, 13, WPS, 3>>(p, st, launches);
+    if (L <= 31) return launch_strip<StripCfg<PP, SS, TRY, D, 13, WPS, 4>>(p, st, launches);
+    return launch_strip<StripCfg<PP, SS, TRY, D, 13, WPS, 5>>(p, st, launches);
+}
+
 static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok) {
     *ok = true;
-#define GBM3D_CASE(PP, SS, TRY, D)                                                             \
-    case PP * 100 + SS:                                                                        \
-        return p.cb == 11 ? launch_strip<StripCfg<PP, SS, TRY, D, 11>>(p, st, launches)       \
-                          : launch_strip<StripCfg<PP, SS, TRY, D, 13>>(p, st, launches);
-    static const bool solo = [] {
-        const char* v = getenv("GBM3D_STRIP_SOLO");  // tuning knob (experiments only)
-        return v && v[0] == '1';
-    }();
-    if (solo && p.P == 8 && p.S == 3)
-        return p.cb == 11 ? launch_strip<StripCfg<8, 3, 4, 8, 11, 1>>(p, st, launches)
-                          : launch_strip<StripCfg<8, 3, 4, 8, 13, 1>>(p, st, launches);
     switch (p.P * 100 + p.S) {
-        GBM3D_CASE(8, 3, 8, 5)
-        GBM3D_CASE(12, 4, 4, 4)
-        GBM3D_CASE(8, 2, 8, 5)
-        GBM3D_CASE(8, 4, 6, 4)
+        case 803: return launch_shape<8, 3, 4, 8, 1>(p, st, launches);     // solo warps
+        case 1204: return launch_shape<12, 4, 4, 4, 2>(p, st, launches);
+        case 802: return launch_shape<8, 2, 8, 5, 2>(p, st, launches);
+        case 804: return launch_shape<8, 4, 6, 4, 2>(p, st, launches);
         default: *ok = false; return cudaSuccess;
     }
-#undef GBM3D_CASE
 }
 
 static int grid_count(int L, int P, int S) { return (L - P) / S + 1 + (((L - P) % S) ? 1 : 0); }

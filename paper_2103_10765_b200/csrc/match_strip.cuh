@@ -33,9 +33,11 @@ namespace gbm3d {
 
 constexpr int HEAP_STRIDE = 33;  // words per heap row: conflict-free per-lane AND per-ref access
 
-template <int P_, int S_, int TRY_, int D_, int CB_, int WPS_ = 2>
+template <int P_, int S_, int TRY_, int D_, int CB_, int WPS_ = 2, int LV_ = 4>
 struct StripCfg {
     static constexpr int P = P_, S = S_, TRY = TRY_, D = D_;
+    static constexpr int LV = LV_;                // heap sift levels: heap = 2^(LV+1) - 1 slots
+    static constexpr int LP = (2 << LV_) - 1;
     static constexpr int WPS = WPS_;  // warps per strip: 2 = paired (shared heaps), 1 = solo
     static constexpr int CB = CB_;  // key = d << CB | code; 2^CB > (2r+1)^2
     static constexpr int Q = P / S, REM = P % S;
@@ -68,12 +70,13 @@ __host__ __device__ inline int heap_levels(int npad) {  // sift levels = h - 1
 struct StripSmem {
     int pitch, rows, img_bytes, heap_words, queue_words, count_bytes;
     __host__ __device__ static StripSmem make(int COLS, int S, int P, int TRY, int D, int NS, int r,
-                                              int K, int WPS) {
+                                              int K, int WPS, int LP) {
         StripSmem g;
         g.pitch = (COLS + 2 * r + 1) & ~1;
         g.rows = S * (TRY * NS - 1) + P + 2 * r + (D - 1);  // + D-1 rows read by the dy tail block
         g.img_bytes = ((g.rows * g.pitch * 2) + 15) & ~15;
-        g.heap_words = NS * TRY * heap_pad(K - 1) * HEAP_STRIDE;
+        g.heap_words = NS * TRY * LP * HEAP_STRIDE;
+        (void)K;
         g.queue_words = WPS * NS * TRY * D * 32;
         g.count_bytes = WPS * NS * TRY * 32;
         return g;
@@ -86,23 +89,24 @@ struct StripSmem {
 // Max-heap (perfect tree, `levels` = h - 1) of one reference: slot i at byte offset i * ROWB
 // from Hb.  Replace the root by key (key < root) and sift down, branch-free, fixed depth.
 constexpr int HEAP_ROWB = HEAP_STRIDE * 4;
-static __device__ __forceinline__ void heap_replace_root(char* Hb, int levels, uint32_t key) {
-    uint32_t o = 0;
+template <int LEVELS>
+static __device__ __forceinline__ void heap_replace_root(char* Hb, uint32_t key) {
+    // absolute shared addresses: child(a) = 2a - Hb + ROWB, sibling = child + ROWB
+    char* a = Hb;
+    const ptrdiff_t cofs = HEAP_ROWB - reinterpret_cast<ptrdiff_t>(Hb);
 #pragma unroll
-    for (int lv = 0; lv < 6; ++lv) {
-        if (lv < levels) {
-            const uint32_t oc = 2 * o + HEAP_ROWB;  // left child of slot o / ROWB
-            const uint32_t v1 = *reinterpret_cast<const uint32_t*>(Hb + oc);
-            const uint32_t v2 = *reinterpret_cast<const uint32_t*>(Hb + oc + HEAP_ROWB);
-            const bool right = v2 > v1;
-            const uint32_t big = right ? v2 : v1;
-            const bool go = big > key;
-            *reinterpret_cast<uint32_t*>(Hb + o) = go ? big : key;
-            const uint32_t on = right ? oc + HEAP_ROWB : oc;
-            o = go ? on : o;
-        }
+    for (int lv = 0; lv < LEVELS; ++lv) {
+        char* const c = reinterpret_cast<char*>(2 * reinterpret_cast<ptrdiff_t>(a) + cofs);
+        const uint32_t v1 = *reinterpret_cast<const uint32_t*>(c);
+        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(c + HEAP_ROWB);
+        const bool right = v2 > v1;
+        const uint32_t big = right ? v2 : v1;
+        const bool go = big > key;
+        *reinterpret_cast<uint32_t*>(a) = go ? big : key;
+        char* const nx = right ? c + HEAP_ROWB : c;
+        a = go ? nx : a;
     }
-    *reinterpret_cast<uint32_t*>(Hb + o) = key;
+    *reinterpret_cast<uint32_t*>(a) = key;
 }
 
 // In-place heapsort of a max-heap of n keys -> ascending order.
@@ -148,8 +152,8 @@ template <class Cfg>
 __device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, int pitch, int brow,
                                             int bcol, const int (&a)[Cfg::NR][Cfg::S],
                                             const int (&tdr)[Cfg::TRY], uint32_t* (&qp)[Cfg::TRY],
-                                            const uint32_t (&mk)[Cfg::TRY], uint32_t code0,
-                                            uint32_t side) {
+                                            const uint32_t (&mk)[Cfg::TRY],
+                                            const uint32_t (&codej)[Cfg::D]) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
     constexpr int Q = Cfg::Q, REM = Cfg::REM, NCH = Cfg::NCH;
     int Cc[D][NCH][S];
@@ -194,7 +198,7 @@ __device__ __forceinline__ void strip_block(const int16_t* __restrict__ sm_img, 
                 // gate: one compare with the heap-root copy, AND the border/self mask bit
                 const bool pass = (d <= tdr[k]) && ((mk[k] >> j) & 1u);
                 if (pass) {
-                    *qp[k] = ((uint32_t)d << Cfg::CB) + (code0 + (uint32_t)j * side);
+                    *qp[k] = ((uint32_t)d << Cfg::CB) + codej[j];
                     qp[k] += 32;
                 }
             }
@@ -263,9 +267,8 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int r = p.r;
     const int L = p.K - 1;
-    const int LP = heap_pad(L);          // heap slots (perfect tree)
-    const int LV = heap_levels(LP);      // sift levels
-    const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K, WPS);
+    constexpr int LP = Cfg::LP;          // heap slots (perfect tree; >= K-1, checked on host)
+    const StripSmem g = StripSmem::make(Cfg::COLS, S, P, TRY, D, NS, r, p.K, WPS, LP);
     int16_t* sm_img = reinterpret_cast<int16_t*>(smem_raw);
     uint32_t* sm_heap = reinterpret_cast<uint32_t*>(smem_raw + g.img_bytes);
     uint32_t* sm_q = sm_heap + g.heap_words;
@@ -369,7 +372,10 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                         mk[k] = jx & ym;
                     }
                 }
-                strip_block<Cfg>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, code0, side);
+                uint32_t codej[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) codej[j] = code0 + (uint32_t)j * side;
+                strip_block<Cfg>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, codej);
             }
             // publish queue lengths; this warp merges reference rows k = half (mod 2)
 #pragma unroll
@@ -407,7 +413,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                     for (int t = 0; t < T; ++t) {
                         const uint32_t key = q[i * 32];
                         if (key < thr) {
-                            heap_replace_root(Hb, LV, key);
+                            heap_replace_root<Cfg::LV>(Hb, key);
                             thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
                         }
                         if (++i == n) {
@@ -496,6 +502,7 @@ template <class Cfg>
 cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launches) {
     const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
     if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
+    if (p.K - 1 > Cfg::LP) return cudaErrorInvalidValue;  // dispatcher picks LV with 2^(LV+1)-1 >= K-1
     int dev = 0, max_optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -505,7 +512,7 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     int best_ns = 0, best_warps = -1, best_smem = 0;
     for (int ns : {4 / Cfg::WPS, 2 / Cfg::WPS, 1}) {
         const int smem = StripSmem::make(Cfg::COLS, Cfg::S, Cfg::P, Cfg::TRY, Cfg::D, ns, p.r, p.K,
-                                         Cfg::WPS).bytes();
+                                         Cfg::WPS, Cfg::LP).bytes();
         if (smem > max_optin) continue;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
@@ -528,10 +535,15 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     return cudaGetLastError();
 }
 
-#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D, WPS)                                             \
-    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 11, WPS>>(const MatchParams&,  \
-                                                                      cudaStream_t, int*);  \
-    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 13, WPS>>(const MatchParams&,  \
-                                                                      cudaStream_t, int*);
+#define GBM3D_INSTANTIATE_STRIP_LV(P, S, TRY, D, WPS, LV)                                      \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 11, WPS, LV>>(const MatchParams&, \
+                                                                          cudaStream_t, int*); \
+    template cudaError_t launch_strip<StripCfg<P, S, TRY, D, 13, WPS, LV>>(const MatchParams&, \
+                                                                          cudaStream_t, int*);
+// heaps of 15 / 31 / 63 slots: K <= 16, K <= 32, K <= 64
+#define GBM3D_INSTANTIATE_STRIP(P, S, TRY, D, WPS)  \
+    GBM3D_INSTANTIATE_STRIP_LV(P, S, TRY, D, WPS, 3) \
+    GBM3D_INSTANTIATE_STRIP_LV(P, S, TRY, D, WPS, 4) \
+    GBM3D_INSTANTIATE_STRIP_LV(P, S, TRY, D, WPS, 5)
 
 }  // namespace gbm3d

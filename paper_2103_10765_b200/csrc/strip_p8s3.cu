@@ -1,6 +1,5 @@
-// Fast-path instantiation: patch 8, stride 3 (TRY=8 reference rows per strip, D=5 dy per block).
+// Fast-path instantiation: patch 8, stride 3 (solo warps: TRY=4 reference rows, D=8 dy per block).
 #include "match_strip.cuh"
 namespace gbm3d {
-GBM3D_INSTANTIATE_STRIP(8, 3, 8, 5, 2)
 GBM3D_INSTANTIATE_STRIP(8, 3, 4, 8, 1)
 }  // namespace gbm3d
