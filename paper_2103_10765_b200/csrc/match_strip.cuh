@@ -78,7 +78,7 @@ struct StripSmem {
         g.heap_words = NS * TRY * LP * HEAP_STRIDE;
         (void)K;
         g.queue_words = WPS * NS * TRY * D * 32;
-        g.count_bytes = WPS * NS * TRY * 32;
+        g.count_bytes = WPS * NS * TRY * 32 * 2;  // pair mode: u8 lengths; solo: u16 task list
         return g;
     }
     __host__ __device__ int bytes() const {
@@ -89,24 +89,41 @@ struct StripSmem {
 // Max-heap (perfect tree, `levels` = h - 1) of one reference: slot i at byte offset i * ROWB
 // from Hb.  Replace the root by key (key < root) and sift down, branch-free, fixed depth.
 constexpr int HEAP_ROWB = HEAP_STRIDE * 4;
+static __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+static __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+static __device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Returns the new root.
 template <int LEVELS>
-static __device__ __forceinline__ void heap_replace_root(char* Hb, uint32_t key) {
-    // absolute shared addresses: child(a) = 2a - Hb + ROWB, sibling = child + ROWB
-    char* a = Hb;
-    const ptrdiff_t cofs = HEAP_ROWB - reinterpret_cast<ptrdiff_t>(Hb);
+static __device__ __forceinline__ uint32_t heap_replace_root(uint32_t base, uint32_t key) {
+    // 32-bit shared addresses: child(a) = 2a - base + ROWB, sibling = child + ROWB
+    const uint32_t cofs = HEAP_ROWB - base;
+    uint32_t a = base;
+    uint32_t root = key;
 #pragma unroll
     for (int lv = 0; lv < LEVELS; ++lv) {
-        char* const c = reinterpret_cast<char*>(2 * reinterpret_cast<ptrdiff_t>(a) + cofs);
-        const uint32_t v1 = *reinterpret_cast<const uint32_t*>(c);
-        const uint32_t v2 = *reinterpret_cast<const uint32_t*>(c + HEAP_ROWB);
+        const uint32_t c = 2 * a + cofs;
+        const uint32_t v1 = lds32(c);
+        const uint32_t v2 = lds32(c + HEAP_ROWB);
         const bool right = v2 > v1;
         const uint32_t big = right ? v2 : v1;
         const bool go = big > key;
-        *reinterpret_cast<uint32_t*>(a) = go ? big : key;
-        char* const nx = right ? c + HEAP_ROWB : c;
+        const uint32_t w = go ? big : key;
+        if (lv == 0) root = w;
+        sts32(a, w);
+        const uint32_t nx = right ? c + HEAP_ROWB : c;
         a = go ? nx : a;
     }
-    *reinterpret_cast<uint32_t*>(a) = key;
+    sts32(a, key);
+    return root;
 }
 
 // In-place heapsort of a max-heap of n keys -> ascending order.
@@ -377,6 +394,48 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                 for (int j = 0; j < D; ++j) codej[j] = code0 + (uint32_t)j * side;
                 strip_block<Cfg>(sm_img, g.pitch, brow, bcol, a, tdr, qp, mk, codej);
             }
+            if constexpr (WPS == 1) {
+                // Solo merge with work redistribution: the warp lists its non-empty queues
+                // (one task = one heap and its queue) and lane t takes tasks t, t+32, ...  so the
+                // sifts are spread evenly over the lanes instead of following the reference
+                // that owns them.
+                uint16_t* const tl = reinterpret_cast<uint16_t*>(sm_cnt) + warp * TRY * 32;
+                const uint32_t ltm = (1u << lane) - 1u;
+                int E = 0;
+#pragma unroll
+                for (int k = 0; k < TRY; ++k) {
+                    const int q = (int)((qp[k] - (qw + k * D * 32)) >> 5);
+                    qp[k] = qw + k * D * 32;
+                    const uint32_t m = __ballot_sync(0xffffffffu, q > 0);
+                    if (q > 0) tl[E + __popc(m & ltm)] = (uint16_t)((k << 9) | (lane << 4) | q);
+                    E += __popc(m);
+                }
+                __syncwarp();
+                const uint32_t heapw = smem_addr(sm_heap + (strip * TRY) * LP * HEAP_STRIDE);
+                const uint32_t qbase = smem_addr(sm_q + (warp * TRY * D) * 32);
+#pragma unroll 1
+                for (int t = lane; t < E; t += 32) {
+                    const uint32_t task = tl[t];
+                    const uint32_t k = task >> 9, l = (task >> 4) & 31u, q = task & 15u;
+                    const uint32_t hb = heapw + (k * LP * HEAP_STRIDE + l) * 4;
+                    uint32_t qa = qbase + (k * D * 32 + l) * 4;
+                    uint32_t thr = min(lds32(hb), p.thr0);
+#pragma unroll 1
+                    for (uint32_t i = 0; i < q; ++i, qa += 128) {
+                        const uint32_t key = lds32(qa);
+                        if (key < thr) thr = min(heap_replace_root<Cfg::LV>(hb, key), p.thr0);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < TRY; ++k) {
+                    if (refok[k]) {
+                        const uint32_t thr = min(heap0[k * LP * HEAP_STRIDE], p.thr0);
+                        tdr[k] = thr == p.thr0 ? p.tdr0 : (int)(thr >> CB);
+                    }
+                }
+                continue;
+            }
             // publish queue lengths; this warp merges reference rows k = half (mod 2)
 #pragma unroll
             for (int k = 0; k < TRY; ++k) {
@@ -407,15 +466,12 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                     int gq = __ffs(nonempty) - 1;
                     int n = (packed >> (4 * gq)) & 15u, i = 0;
                     int k = half + WPS * (gq / WPS), col = (lane + 5 * k) & 31;
-                    char* Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
+                    uint32_t Hb = smem_addr(heapb + (k * LP * HEAP_STRIDE + col) * 4);
                     const uint32_t* q = sm_q + (((warp ^ (gq % WPS)) * TRY + k) * D) * 32 + col;
-                    uint32_t thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
+                    uint32_t thr = min(lds32(Hb), p.thr0);
                     for (int t = 0; t < T; ++t) {
                         const uint32_t key = q[i * 32];
-                        if (key < thr) {
-                            heap_replace_root<Cfg::LV>(Hb, key);
-                            thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
-                        }
+                        if (key < thr) thr = min(heap_replace_root<Cfg::LV>(Hb, key), p.thr0);
                         if (++i == n) {
                             nonempty &= ~(1u << gq);
                             if (nonempty) {
@@ -424,9 +480,9 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
                                 i = 0;
                                 k = half + WPS * (gq / WPS);
                                 col = (lane + 5 * k) & 31;
-                                Hb = heapb + (k * LP * HEAP_STRIDE + col) * 4;
+                                Hb = smem_addr(heapb + (k * LP * HEAP_STRIDE + col) * 4);
                                 q = sm_q + (((warp ^ (gq % WPS)) * TRY + k) * D) * 32 + col;
-                                thr = min(*reinterpret_cast<uint32_t*>(Hb), p.thr0);
+                                thr = min(lds32(Hb), p.thr0);
                             }
                         }
                     }
