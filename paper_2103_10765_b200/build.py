@@ -13,6 +13,12 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgbm3d.so")
 BUILD = os.path.join(PKG, "build")
+# Dev experiments only: GBM3D_NVCC_EXTRA adds nvcc flags and GBM3D_LIB_OUT redirects the output
+# (e.g. variants/libgbm3d_x.so, loaded via GBM3D_LIB); the default build ignores both.
+EXTRA = os.environ.get("GBM3D_NVCC_EXTRA", "").split()
+if os.environ.get("GBM3D_LIB_OUT"):
+    LIB = os.path.abspath(os.environ["GBM3D_LIB_OUT"])
+    BUILD = "/tmp/gbm3d_objs_" + os.path.basename(LIB)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
@@ -37,7 +43,7 @@ def up_to_date() -> bool:
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
