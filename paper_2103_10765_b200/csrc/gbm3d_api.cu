@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "match_direct.cuh"
 #include "match_strip.cuh"
+#include "match_tc.cuh"
 
 namespace gbm3d {
 
@@ -37,6 +38,19 @@ static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* la
         case 804: return launch_shape<8, 4, 6, 4, 2>(p, st, launches);
         default: *ok = false; return cudaSuccess;
     }
+}
+
+// Tensor-core product-form kernel (match_tc.cuh): patch 8, stride 3, the tile's candidate
+// columns 7S + 2r + 1 <= 64 (radius <= 21), 2 <= K <= 32.
+extern template cudaError_t launch_tc<3, 15>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tc<3, 31>(const MatchParams&, cudaStream_t, int*);
+static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok) {
+    *ok = false;
+    if (p.P != 8 || p.S != 3 || 7 * p.S + 2 * p.r + 1 > tcm::NB || p.K < 2 || p.K > 32)
+        return cudaSuccess;
+    *ok = true;
+    if (p.K - 1 <= 15) return launch_tc<3, 15>(p, st, launches);
+    return launch_tc<3, 31>(p, st, launches);
 }
 
 static int grid_count(int L, int P, int S) { return (L - P) / S + 1 + (((L - P) % S) ? 1 : 0); }
@@ -103,7 +117,11 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
     bool fast = false;
-    if (method == GBM3D_METHOD_PRODUCT) return GBM3D_ERR_UNSUPPORTED;
+    if (method == GBM3D_METHOD_PRODUCT) {
+        e = tc_dispatch(p, st, &launches, &fast);
+        if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (!fast) return GBM3D_ERR_UNSUPPORTED;
+    }
     if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_SSD) {
         e = strip_dispatch(p, st, &launches, &fast);
         if (e != cudaSuccess) return GBM3D_ERR_CUDA;
