@@ -36,9 +36,13 @@ constexpr int TY = 16, TX = 8;  // reference tile (grid rows x grid cols) = 128 
 constexpr int NB = 64;          // candidate columns per MMA tile (N)
 constexpr int PC = 72;          // byte-plane pitch: 64 candidate columns + 7 + pad
 constexpr int NSTG = 4;         // B-operand ring stages
-constexpr int EPI_WARPS = 4, MMA_WARP = 4, BLD_WARP0 = 5, NBLD = 2;
-constexpr int THREADS = 32 * (EPI_WARPS + 1 + NBLD);
-constexpr int STG_PITCH = 68;   // epilogue staging words per lane (64 + 4: conflict-free STS.128)
+// warps 0-3: epilogue (TMEM -> e = d - gate, window masks, staged rows); 4-7: selectors (one
+// per epilogue warp, same lane <-> reference map; register top-(K-1) lists); 8: MMA issuer;
+// 9-10: B builders
+constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, BLD_WARP0 = 9, NBLD = 2;
+constexpr int THREADS = 32 * 11;
+constexpr int NSLOT = 2;        // staged rows in flight per epilogue/selector pair
+constexpr int STG_PITCH = 68;   // words per lane and staged row: e[64], mask lo/hi, gate, row
 constexpr int A_BYTES = 128 * 64, B_BYTES = 64 * 64;  // one byte plane of A / of a B stage
 constexpr uint32_t TMEM_COLS = 512;                   // 2 stages x (hh, mid, ll) x 64
 }  // namespace tcm
@@ -59,8 +63,10 @@ struct TcGeom {
         g.off_lo = g.off_hi + ((g.PR * PC + 15) & ~15);
         g.off_nc = g.off_lo + ((g.PR * PC + 15) & ~15);  // candidate norms [NT][64]
         g.off_stg = g.off_nc + g.NT * NB * 4;           // epilogue staging / prologue scratch
-        g.off_bar = g.off_stg + EPI_WARPS * 32 * STG_PITCH * 4;
-        g.total = g.off_bar + (2 * NSTG + 4) * 8 + 16;
+        g.off_bar = g.off_stg + EPI_WARPS * NSLOT * 32 * STG_PITCH * 4;
+        // mbarriers: full/empty[NSTG], tfull/tempty[2], sfull/sempty[EPI_WARPS*NSLOT]; then the
+        // published gates [EPI_WARPS*32] and the TMEM address
+        g.total = g.off_bar + (2 * NSTG + 4 + 2 * EPI_WARPS * NSLOT) * 8 + EPI_WARPS * 32 * 4 + 16;
         return g;
     }
 };
@@ -87,9 +93,23 @@ static __device__ __forceinline__ void list_insert(uint32_t (&L)[KL], uint32_t x
     L[0] = min(L[0], x);
 }
 
-// i-th candidate row of the front/back interleaved order over [lo, hi].
-static __device__ __forceinline__ int tc_row(int s, int lo, int hi) {
-    return (s & 1) ? hi - (s >> 1) : lo + (s >> 1);
+// Candidate rows are visited in a scrambled order t = lo + (s * step) mod n, step coprime to n
+// near 0.618 n: spatially ordered visits (raster, centre-out) let the smooth image content
+// keep the gates loose, a spread order fills the lists with typical distances early.
+static __device__ __forceinline__ int tc_step(int n) {
+    int st = max(1, (int)(0.618f * (float)n));
+    for (;; ++st) {
+        int x = st, y = n;
+        while (y) {
+            const int t = x % y;
+            x = y;
+            y = t;
+        }
+        if (x == 1) return st;
+    }
+}
+static __device__ __forceinline__ int tc_row(int s, int lo, int n, int step) {
+    return lo + (int)(((long long)s * step) % n);
 }
 
 // Exact per-reference recomputation with 64-bit keys from global memory (rare: only when tau
@@ -164,12 +184,17 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
     uint64_t* const empty = bars + NSTG;       // MMA commit -> builders
     uint64_t* const tfull = bars + 2 * NSTG;   // MMA commit -> epilogue
     uint64_t* const tempty = tfull + 2;        // epilogue -> MMA   (count EPI_WARPS)
-    uint32_t* const tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* const sfull = tempty + 2;                // epilogue warp w -> selector w
+    uint64_t* const sempty = sfull + EPI_WARPS * NSLOT;  // selector w -> epilogue warp w
+    volatile uint32_t* const gate_pub =
+        reinterpret_cast<volatile uint32_t*>(sempty + EPI_WARPS * NSLOT);
+    uint32_t* const tslot = reinterpret_cast<uint32_t*>(sempty + EPI_WARPS * NSLOT) + EPI_WARPS * 32;
 
     // valid candidate rows / columns of the tile (candidates lie fully inside the image)
     const int t_lo = max(0, -gy0), t_hi = min(g.NT - 1, (p.H - P) - gy0);
     const int j_lo = max(0, -gx0), j_hi = min(g.NJ - 1, (p.W - P) - gx0);
     const int nseq = t_hi - t_lo + 1;
+    const int step = tc_step(nseq);
 
     // ---- prologue 1: pixel tile -> byte planes of z' = z + 32768, and z'^2 (mod 2^32)
     {
@@ -195,9 +220,14 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                 tc::mbar_init(&tfull[i], 1);
                 tc::mbar_init(&tempty[i], EPI_WARPS);
             }
+            for (int i = 0; i < EPI_WARPS * NSLOT; ++i) {
+                tc::mbar_init(&sfull[i], 1);
+                tc::mbar_init(&sempty[i], 1);
+            }
             tc::fence_mbar_init();
         }
         if (warp == MMA_WARP) tc::tmem_alloc<TMEM_COLS>(tslot);
+        if (threadIdx.x < EPI_WARPS * 32) gate_pub[threadIdx.x] = (uint32_t)(p.tdr0 + 1);
         __syncthreads();
         // horizontal sums of squares over the 8 patch columns (scratch in the B ring)
         uint32_t* hs = reinterpret_cast<uint32_t*>(sm + g.off_b);
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
         for (int s = 0; s < nseq; ++s) {
             const int stage = s % NSTG;
             if (s >= NSTG) tc::mbar_wait(&empty[stage], ((s / NSTG) - 1) & 1);
-            const int t = tc_row(s, t_lo, t_hi);
+            const int t = tc_row(s, t_lo, nseq, step);
             uint8_t* const bh = sm + g.off_b + stage * 2 * B_BYTES;
             uint8_t* const bl = bh + B_BYTES;
 #pragma unroll
@@ -297,33 +327,40 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
         }
         __syncwarp();
     } else {
-        // ---- epilogue warps: keys, window mask, per-lane top-(K-1) network
-        const int a = 4 * warp + (lane >> 3), bb = lane & 7;
+        // ---- epilogue (warps 0-3) and selector (warps 4-7) of lane quarter w
+        const bool is_sel = warp >= SEL_WARP0;
+        const int w = is_sel ? warp - SEL_WARP0 : warp;
+        const int a = 4 * w + (lane >> 3), bb = lane & 7;
         const bool refok = (ky0 + a < kr1) && (kx0 + bb < p.Rx_reg) && (p.K > 1);
         const int ty = r + S * a, tx = r + S * bb;  // reference position in tile coordinates
-        const uint32_t Nr = nc[ty * NB + tx];
-        const int c0 = max(S * bb, j_lo), c1 = min(S * bb + 2 * r, j_hi);
-        const uint64_t cm = (c1 >= c0) ? ((c1 >= 63 ? ~0ull : ((2ull << c1) - 1ull)) &
-                                          ~((1ull << c0) - 1ull))
-                                       : 0ull;
-        const uint32_t cm_lo = (uint32_t)cm, cm_hi = (uint32_t)(cm >> 32);
         const bool warp_active = __any_sync(0xffffffffu, refok);
-        const int wt0 = S * 4 * warp, wt1 = S * (4 * warp + 3) + 2 * r;
+        const int wt0 = S * 4 * w, wt1 = S * (4 * w + 3) + 2 * r;  // rows any lane can use
         const uint32_t side = (uint32_t)p.side;
         const int cb = p.cb;
-        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
-        uint32_t* const stg = reinterpret_cast<uint32_t*>(sm + g.off_stg) + (warp * 32 + lane) * STG_PITCH;
-
-        uint32_t L[KL];
-#pragma unroll
-        for (int i = 0; i < KL; ++i) L[i] = KEY_INF;
-        uint32_t gate = (uint32_t)(p.tdr0 + 1);  // pass iff d < gate
-
-        for (int s = 0; s < nseq; ++s) {
-            const int ts = s & 1;
-            const int t = tc_row(s, t_lo, t_hi);
-            tc::mbar_wait(&tfull[ts], (s >> 1) & 1);
-            if (warp_active && t >= wt0 && t <= wt1) {
+        uint32_t* const stg0 = reinterpret_cast<uint32_t*>(sm + g.off_stg) +
+                               (w * NSLOT * 32 + lane) * STG_PITCH;  // + slot * 32 * STG_PITCH
+        int used = 0;  // staged rows so far (the two warps of the pair count identically)
+        if (!is_sel) {
+            const uint32_t Nr = nc[ty * NB + tx];
+            const int c0 = max(S * bb, j_lo), c1 = min(S * bb + 2 * r, j_hi);
+            const uint64_t cm = (c1 >= c0) ? ((c1 >= 63 ? ~0ull : ((2ull << c1) - 1ull)) &
+                                              ~((1ull << c0) - 1ull))
+                                           : 0ull;
+            const uint32_t cm_lo = (uint32_t)cm, cm_hi = (uint32_t)(cm >> 32);
+            const uint32_t taddr = tmem + ((uint32_t)(32 * w) << 16);
+            for (int s = 0; s < nseq; ++s) {
+                const int ts = s & 1;
+                const int t = tc_row(s, t_lo, nseq, step);
+                tc::mbar_wait(&tfull[ts], (s >> 1) & 1);
+                if (!(warp_active && t >= wt0 && t <= wt1)) {
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                    continue;
+                }
+                const int slot = used % NSLOT;
+                if (used >= NSLOT) tc::mbar_wait(&sempty[w * NSLOT + slot], ((used / NSLOT) - 1) & 1);
+                uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
+                const uint32_t gate = gate_pub[w * 32 + lane];  // selector's latest gate
                 tc::tc_fence_after();
                 const uint32_t cl = Nr - gate;  // e = d - gate = N_c - 2 G + (N_r - gate)
                 uint32_t msk[2] = {0u, 0u};
@@ -370,9 +407,26 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                     if (tx < 32) mlo &= ~(1u << tx);
                     else mhi &= ~(1u << (tx - 32));
                 }
+                *reinterpret_cast<uint4*>(stg + 64) = make_uint4(mlo, mhi, gate, (uint32_t)t);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sfull[w * NSLOT + slot]);
+                ++used;
+            }
+        } else {
+            uint32_t L[KL];
+#pragma unroll
+            for (int i = 0; i < KL; ++i) L[i] = KEY_INF;
+            for (int s = 0; s < nseq; ++s) {
+                const int t = tc_row(s, t_lo, nseq, step);
+                if (!(warp_active && t >= wt0 && t <= wt1)) continue;
+                const int slot = used % NSLOT;
+                tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
+                const uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
+                const uint4 hdr = *reinterpret_cast<const uint4*>(stg + 64);
+                uint32_t mlo = hdr.x, mhi = hdr.y;
+                const uint32_t g0 = hdr.z;
                 const int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
                 const uint32_t code_row = (uint32_t)(t - S * a) * side - (uint32_t)(S * bb);
-                const uint32_t g0 = gate;
                 for (int q = 0; q < R; ++q) {
                     uint32_t key = KEY_INF;
                     if (mlo | mhi) {
@@ -389,67 +443,69 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                     }
                     list_insert<KL>(L, key);
                 }
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sempty[w * NSLOT + slot]);
                 const uint32_t top = L[KL - 1];
                 const int gd = (top == KEY_INF) ? p.tdr0 : min((int)(top >> cb), p.tdr0);
-                gate = (uint32_t)(gd + 1);
-            } else {
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                gate_pub[w * 32 + lane] = (uint32_t)(gd + 1);
+                ++used;
             }
-        }
 
-        // ---- epilogue: slot 0 = self, ranks 1.. = list, pads (self, -1); coalesced rows
-        const int Kout = p.K;
-        const int ry = S * (ky0 + a), rx = S * (kx0 + bb);
-        const int self = ry * p.W + rx;
-        const uint32_t cmask = (1u << cb) - 1u;
-        int cnt = 0;
-        __syncwarp();
-        stg[0] = (uint32_t)self;
-        stg[Kout] = 0u;
+            // ---- output: slot 0 = self, ranks 1.. = list, pads (self, -1); coalesced rows
+            uint32_t* const stg = stg0;  // every staged row has been consumed: reuse slot 0
+            const int Kout = p.K;
+            const int ry = S * (ky0 + a), rx = S * (kx0 + bb);
+            const int self = ry * p.W + rx;
+            const uint32_t cmask = (1u << cb) - 1u;
+            int cnt = 0;
+            __syncwarp();
+            stg[0] = (uint32_t)self;
+            stg[Kout] = 0u;
 #pragma unroll
-        for (int i = 0; i < KL; ++i) {
-            if (i + 1 < Kout) {
-                const uint32_t key = L[i];
-                int32_t vi = self, vd = -1;
-                if (key != KEY_INF) {
-                    const uint32_t code = key & cmask;
-                    const int dy = (int)(code / side) - r, dx = (int)(code % side) - r;
-                    vi = (ry + dy) * p.W + rx + dx;
-                    vd = (int32_t)(key >> cb);
-                    ++cnt;
+            for (int i = 0; i < KL; ++i) {
+                if (i + 1 < Kout) {
+                    const uint32_t key = L[i];
+                    int32_t vi = self, vd = -1;
+                    if (key != KEY_INF) {
+                        const uint32_t code = key & cmask;
+                        const int dy = (int)(code / side) - r, dx = (int)(code % side) - r;
+                        vi = (ry + dy) * p.W + rx + dx;
+                        vd = (int32_t)(key >> cb);
+                        ++cnt;
+                    }
+                    stg[1 + i] = (uint32_t)vi;
+                    stg[Kout + 1 + i] = (uint32_t)vd;
                 }
-                stg[1 + i] = (uint32_t)vi;
-                stg[Kout + 1 + i] = (uint32_t)vd;
             }
-        }
-        __syncwarp();
-        const int64_t ref0 = (int64_t)bimg * p.out_bstride;
-        for (int l = 0; l < 32; ++l) {
-            const int la = 4 * warp + (l >> 3), lb = l & 7;
-            if (ky0 + la >= kr1 || kx0 + lb >= p.Rx_reg) continue;
-            const int64_t ref = ref0 + (int64_t)(ky0 + la - p.row_begin) * p.Rx + (kx0 + lb);
-            const uint32_t* src = reinterpret_cast<uint32_t*>(sm + g.off_stg) + (warp * 32 + l) * STG_PITCH;
-            for (int s2 = lane; s2 < Kout; s2 += 32) {
-                p.idx[ref * Kout + s2] = (int32_t)src[s2];
-                p.dist[ref * Kout + s2] = (int32_t)src[Kout + s2];
+            __syncwarp();
+            const int64_t ref0 = (int64_t)bimg * p.out_bstride;
+            for (int l = 0; l < 32; ++l) {
+                const int la = 4 * w + (l >> 3), lb = l & 7;
+                if (ky0 + la >= kr1 || kx0 + lb >= p.Rx_reg) continue;
+                const int64_t ref = ref0 + (int64_t)(ky0 + la - p.row_begin) * p.Rx + (kx0 + lb);
+                const uint32_t* src = reinterpret_cast<uint32_t*>(sm + g.off_stg) +
+                                      (w * NSLOT * 32 + l) * STG_PITCH;
+                for (int s2 = lane; s2 < Kout; s2 += 32) {
+                    p.idx[ref * Kout + s2] = (int32_t)src[s2];
+                    p.dist[ref * Kout + s2] = (int32_t)src[Kout + s2];
+                }
             }
-        }
-        __syncwarp();  // the warp's row stores above precede a fallback rewrite of the same rows
-        // exact fallback (tau beyond the 32-bit key range and a short list): own reference
-        if (refok && p.tau_above_dsat && cnt < Kout - 1) {
-            const int wy = min(p.H - P, ry + r) - max(0, ry - r) + 1;
-            const int wx = min(p.W - P, rx + r) - max(0, rx - r) + 1;
-            if (cnt < wy * wx - 1) {
+            __syncwarp();  // the warp's row stores above precede a fallback rewrite of the same rows
+            // exact fallback (tau beyond the 32-bit key range and a short list): own reference
+            if (refok && p.tau_above_dsat && cnt < Kout - 1) {
+                const int wy = min(p.H - P, ry + r) - max(0, ry - r) + 1;
+                const int wx = min(p.W - P, rx + r) - max(0, rx - r) + 1;
+                if (cnt < wy * wx - 1) {
+                    const int64_t ref = ref0 + (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
+                    cnt = tc_exact_ref(p.img + (int64_t)bimg * p.img_bstride, p.slab_y0, p.H, p.W,
+                                       P, r, ry, rx, Kout, p.tau, p.idx + ref * Kout,
+                                       p.dist + ref * Kout);
+                }
+            }
+            if (refok && p.nvalid) {
                 const int64_t ref = ref0 + (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
-                cnt = tc_exact_ref(p.img + (int64_t)bimg * p.img_bstride, p.slab_y0, p.H, p.W, P,
-                                   r, ry, rx, Kout, p.tau, p.idx + ref * Kout,
-                                   p.dist + ref * Kout);
+                p.nvalid[ref] = 1 + cnt;
             }
-        }
-        if (refok && p.nvalid) {
-            const int64_t ref = ref0 + (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
-            p.nvalid[ref] = 1 + cnt;
         }
     }
 
