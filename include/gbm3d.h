@@ -65,7 +65,8 @@ enum {
     GBM3D_METHOD_AUTO = 0,     /* fastest exact kernel available for the shape            */
     GBM3D_METHOD_SSD = 1,      /* displacement-organised shifted-difference box sums      */
     GBM3D_METHOD_PRODUCT = 2,  /* Eq. (2) product form: norms + box sums of Z * S_delta Z */
-    GBM3D_METHOD_DIRECT = 3    /* generic per-reference direct SSD (any shape; slow)      */
+    GBM3D_METHOD_DIRECT = 3,   /* generic per-reference direct SSD (any shape; slow)      */
+    GBM3D_METHOD_PRODUCT_I8 = 4 /* product form, byte-plane int8 tensor-core kernel only   */
 };
 
 /* Reference-grid counts along both axes (host, pure, reading R3).

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # GBM3D_LIB: dev override to load an experimental build of the same library.
 _LIB_PATH = os.environ.get("GBM3D_LIB") or os.path.join(_HERE, "libgbm3d.so")
 TAU_NONE = (1 << 63) - 1  # GBM3D_TAU_NONE
-METHODS = {"auto": 0, "ssd": 1, "product": 2, "direct": 3}
+METHODS = {"auto": 0, "ssd": 1, "product": 2, "direct": 3, "product_i8": 4}
 _ERR = {0: "ok", -1: "GBM3D_ERR_ARG", -2: "GBM3D_ERR_RANGE", -3: "GBM3D_ERR_UNSUPPORTED",
         -4: "GBM3D_ERR_CUDA"}
 _lib = None

@@ -8,7 +8,7 @@
 #include "common.cuh"
 #include "match_direct.cuh"
 #include "match_strip.cuh"
-#include "match_tc.cuh"
+#include "match_tc16.cuh"
 
 namespace gbm3d {
 
@@ -40,17 +40,26 @@ static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* la
     }
 }
 
-// Tensor-core product-form kernel (match_tc.cuh): patch 8, stride 3, the tile's candidate
-// columns 7S + 2r + 1 <= 64 (radius <= 21), 2 <= K <= 32.
-extern template cudaError_t launch_tc<3, 15>(const MatchParams&, cudaStream_t, int*);
-extern template cudaError_t launch_tc<3, 31>(const MatchParams&, cudaStream_t, int*);
-static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok) {
+// Tensor-core product-form kernels: patch 8, stride 3, the tile's candidate columns
+// 7S + 2r + 1 <= 64 (radius <= 21), 2 <= K <= 32.  PRODUCT = fp16 kernel (match_tc16.cuh) with
+// the exact int8 kernel (match_tc.cuh) redoing tiles outside the fp16 range bound;
+// PRODUCT_I8 = the int8 kernel alone.
+extern template cudaError_t launch_tc<3, 15>(const MatchParams&, cudaStream_t, int*, int);
+extern template cudaError_t launch_tc<3, 31>(const MatchParams&, cudaStream_t, int*, int);
+extern template cudaError_t launch_tc16<3, 15>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tc16<3, 31>(const MatchParams&, cudaStream_t, int*);
+static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok,
+                               bool int8_only) {
     *ok = false;
     if (p.P != 8 || p.S != 3 || 7 * p.S + 2 * p.r + 1 > tcm::NB || p.K < 2 || p.K > 32)
         return cudaSuccess;
     *ok = true;
-    if (p.K - 1 <= 15) return launch_tc<3, 15>(p, st, launches);
-    return launch_tc<3, 31>(p, st, launches);
+    if (int8_only) {
+        if (p.K - 1 <= 15) return launch_tc<3, 15>(p, st, launches, 0);
+        return launch_tc<3, 31>(p, st, launches, 0);
+    }
+    if (p.K - 1 <= 15) return launch_tc16<3, 15>(p, st, launches);
+    return launch_tc16<3, 31>(p, st, launches);
 }
 
 static int grid_count(int L, int P, int S) { return (L - P) / S + 1 + (((L - P) % S) ? 1 : 0); }
@@ -117,8 +126,8 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
     bool fast = false;
-    if (method == GBM3D_METHOD_PRODUCT) {
-        e = tc_dispatch(p, st, &launches, &fast);
+    if (method == GBM3D_METHOD_PRODUCT || method == GBM3D_METHOD_PRODUCT_I8) {
+        e = tc_dispatch(p, st, &launches, &fast, method == GBM3D_METHOD_PRODUCT_I8);
         if (e != cudaSuccess) return GBM3D_ERR_CUDA;
         if (!fast) return GBM3D_ERR_UNSUPPORTED;
     }
@@ -178,7 +187,7 @@ int gbm3d_block_match_ex(const int16_t* imgs, int B, int H, int W, int patch, in
                          int radius, int K, int64_t tau, int method, int32_t* idx,
                          int32_t* dist, int32_t* n_valid, void* stream) {
     if (!imgs || !idx || !dist) return GBM3D_ERR_ARG;
-    if (method < GBM3D_METHOD_AUTO || method > GBM3D_METHOD_DIRECT) return GBM3D_ERR_ARG;
+    if (method < GBM3D_METHOD_AUTO || method > GBM3D_METHOD_PRODUCT_I8) return GBM3D_ERR_ARG;
     MatchParams p;
     const int st = make_params(p, B, H, W, patch, stride, radius, K, tau);
     if (st != GBM3D_OK) return st;

@@ -31,6 +31,18 @@
 
 namespace gbm3d {
 
+#if GBM3D_TC_TRACE  // dev-only timeline of one CTA (clock64), read by gbm3d_dev_tc_trace
+static __device__ long long g_tc_trace[8192];
+#define TC_TR(i, v)                                                                   \
+    do {                                                                              \
+        if (blockIdx.x == 10 && blockIdx.y == 10 && blockIdx.z == 0) g_tc_trace[i] = (v); \
+    } while (0)
+#else
+#define TC_TR(i, v) \
+    do {            \
+    } while (0)
+#endif
+
 namespace tcm {
 constexpr int TY = 16, TX = 8;  // reference tile (grid rows x grid cols) = 128 MMA rows
 constexpr int NB = 64;          // candidate columns per MMA tile (N)
@@ -41,7 +53,7 @@ constexpr int NSTG = 4;         // B-operand ring stages
 // 9-10: B builders
 constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, BLD_WARP0 = 9, NBLD = 2;
 constexpr int THREADS = 32 * 11;
-constexpr int NSLOT = 2;        // staged rows in flight per epilogue/selector pair
+constexpr int NSLOT = 4;        // staged rows in flight per epilogue/selector pair
 constexpr int STG_PITCH = 68;   // words per lane and staged row: e[64], mask lo/hi, gate, row
 constexpr int A_BYTES = 128 * 64, B_BYTES = 64 * 64;  // one byte plane of A / of a B stage
 constexpr uint32_t TMEM_COLS = 512;                   // 2 stages x (hh, mid, ll) x 64
@@ -108,8 +120,10 @@ static __device__ __forceinline__ int tc_step(int n) {
         if (x == 1) return st;
     }
 }
-static __device__ __forceinline__ int tc_row(int s, int lo, int n, int step) {
-    return lo + (int)(((long long)s * step) % n);
+// Running form: off_{s+1} = (off_s + step) mod n, off_0 = 0; row = lo + off.
+static __device__ __forceinline__ int tc_next(int off, int n, int step) {
+    off += step;
+    return off >= n ? off - n : off;
 }
 
 // Exact per-reference recomputation with 64-bit keys from global memory (rare: only when tau
@@ -162,8 +176,13 @@ static __device__ __noinline__ int tc_exact_ref(const int16_t* __restrict__ img,
     return cnt;
 }
 
+// Tile marker written by the fp16 kernel (match_tc16.cuh) into the slot-0 distance of the
+// tile's first reference when the tile's pixel range is outside its exactness bound; the int8
+// kernel launched with only_marked = 1 recomputes exactly those tiles.
+constexpr int32_t TC_TILE_MARK = -2;
+
 template <int S, int KL>
-__global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p) {
+__global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p, int only_marked) {
     using namespace tcm;
     extern __shared__ __align__(1024) unsigned char sm[];
     const TcGeom g = TcGeom::make(S, p.r);
@@ -173,6 +192,10 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
     const int bimg = blockIdx.z;
     const int kr1 = min(p.row_end, p.Ry_reg);
     const int ky0 = p.row_begin + (int)blockIdx.y * TY, kx0 = (int)blockIdx.x * TX;
+    if (only_marked) {
+        const int64_t ref = (int64_t)bimg * p.out_bstride + (int64_t)(ky0 - p.row_begin) * p.Rx + kx0;
+        if (p.dist[ref * p.K] != TC_TILE_MARK) return;
+    }
     const int gy0 = S * ky0 - r, gx0 = S * kx0 - r;  // global pixel of tile (0, 0)
     const int16_t* __restrict__ img = p.img + (int64_t)bimg * p.img_bstride;
 
@@ -264,14 +287,16 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
         tc::tc_fence_after();
     }
     const uint32_t tmem = *tslot;
+    if (threadIdx.x == 0) TC_TR(0, clock64());
 
     if (warp >= BLD_WARP0) {
         // ---- B builders: candidate row t -> 64 candidate patches, canonical K-major
         const int n = threadIdx.x - 32 * BLD_WARP0;  // candidate column 0..63
-        for (int s = 0; s < nseq; ++s) {
+        int off = 0;
+        for (int s = 0; s < nseq; ++s, off = tc_next(off, nseq, step)) {
             const int stage = s % NSTG;
             if (s >= NSTG) tc::mbar_wait(&empty[stage], ((s / NSTG) - 1) & 1);
-            const int t = tc_row(s, t_lo, nseq, step);
+            const int t = t_lo + off;
             uint8_t* const bh = sm + g.off_b + stage * 2 * B_BYTES;
             uint8_t* const bl = bh + B_BYTES;
 #pragma unroll
@@ -323,6 +348,7 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                 }
                 tc::mma_commit(&empty[stage]);
                 tc::mma_commit(&tfull[ts]);
+                TC_TR(16 + s, clock64());
             }
         }
         __syncwarp();
@@ -348,10 +374,12 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                                            : 0ull;
             const uint32_t cm_lo = (uint32_t)cm, cm_hi = (uint32_t)(cm >> 32);
             const uint32_t taddr = tmem + ((uint32_t)(32 * w) << 16);
-            for (int s = 0; s < nseq; ++s) {
+            int off = 0;
+            for (int s = 0; s < nseq; ++s, off = tc_next(off, nseq, step)) {
                 const int ts = s & 1;
-                const int t = tc_row(s, t_lo, nseq, step);
+                const int t = t_lo + off;
                 tc::mbar_wait(&tfull[ts], (s >> 1) & 1);
+                if (lane == 0) TC_TR(1000 + w * 200 + s, clock64());
                 if (!(warp_active && t >= wt0 && t <= wt1)) {
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&tempty[ts]);
@@ -410,45 +438,96 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
                 *reinterpret_cast<uint4*>(stg + 64) = make_uint4(mlo, mhi, gate, (uint32_t)t);
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sfull[w * NSLOT + slot]);
+                if (lane == 0) TC_TR(2000 + w * 200 + s, clock64());
                 ++used;
             }
         } else {
             uint32_t L[KL];
 #pragma unroll
             for (int i = 0; i < KL; ++i) L[i] = KEY_INF;
-            for (int s = 0; s < nseq; ++s) {
-                const int t = tc_row(s, t_lo, nseq, step);
-                if (!(warp_active && t >= wt0 && t <= wt1)) continue;
-                const int slot = used % NSLOT;
-                tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
-                const uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
-                const uint4 hdr = *reinterpret_cast<const uint4*>(stg + 64);
-                uint32_t mlo = hdr.x, mhi = hdr.y;
-                const uint32_t g0 = hdr.z;
-                const int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
-                const uint32_t code_row = (uint32_t)(t - S * a) * side - (uint32_t)(S * bb);
+            // number of rows the epilogue warp stages (same relevance test, same order)
+            int nrel = 0;
+            if (warp_active) {
+                const int lo = max(wt0, t_lo), hi = min(wt1, t_hi);
+                nrel = hi >= lo ? hi - lo + 1 : 0;
+            }
+            while (used < nrel) {
+                // take every staged row that is ready (at least one): fewer, fuller rounds
+                tc::mbar_wait(&sfull[w * NSLOT + used % NSLOT], (used / NSLOT) & 1);
+                int nb = 1;
+#ifndef GBM3D_TC_BATCH
+#define GBM3D_TC_BATCH 1
+#endif
+                if (GBM3D_TC_BATCH && lane == 0) {
+                    while (nb < NSLOT && used + nb < nrel &&
+                           tc::mbar_test(&sfull[w * NSLOT + (used + nb) % NSLOT],
+                                         ((used + nb) / NSLOT) & 1))
+                        ++nb;
+                }
+                nb = __shfl_sync(0xffffffffu, nb, 0);
+                uint32_t mlo[NSLOT], mhi[NSLOT], g0[NSLOT], crow[NSLOT];
+                int cnt = 0;
+#pragma unroll
+                for (int b2 = 0; b2 < NSLOT; ++b2) {
+                    mlo[b2] = mhi[b2] = 0u;
+                    g0[b2] = crow[b2] = 0u;
+                    if (b2 < nb) {
+                        const uint4 hdr = *reinterpret_cast<const uint4*>(
+                            stg0 + ((used + b2) % NSLOT) * 32 * STG_PITCH + 64);
+                        mlo[b2] = hdr.x;
+                        mhi[b2] = hdr.y;
+                        g0[b2] = hdr.z;
+                        crow[b2] = (uint32_t)((int)hdr.w - S * a) * side - (uint32_t)(S * bb);
+                        cnt += __popc(hdr.x) + __popc(hdr.y);
+                    }
+                }
+                const int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
                 for (int q = 0; q < R; ++q) {
                     uint32_t key = KEY_INF;
-                    if (mlo | mhi) {
+                    // first staged row with a pending candidate
+                    int bsel = -1;
+#pragma unroll
+                    for (int b2 = NSLOT - 1; b2 >= 0; --b2)
+                        if (mlo[b2] | mhi[b2]) bsel = b2;
+                    if (bsel >= 0) {
+                        uint32_t ml = 0, mh = 0, gg = 0, cr = 0;
+#pragma unroll
+                        for (int b2 = 0; b2 < NSLOT; ++b2)
+                            if (b2 == bsel) {
+                                ml = mlo[b2];
+                                mh = mhi[b2];
+                                gg = g0[b2];
+                                cr = crow[b2];
+                            }
                         int j;
-                        if (mlo) {
-                            j = __ffs(mlo) - 1;
-                            mlo &= mlo - 1u;
+                        if (ml) {
+                            j = __ffs(ml) - 1;
+                            ml &= ml - 1u;
                         } else {
-                            j = 31 + __ffs(mhi);
-                            mhi &= mhi - 1u;
+                            j = 31 + __ffs(mh);
+                            mh &= mh - 1u;
                         }
-                        const uint32_t d = stg[j] + g0;
-                        key = (d << cb) | (code_row + (uint32_t)j);
+#pragma unroll
+                        for (int b2 = 0; b2 < NSLOT; ++b2)
+                            if (b2 == bsel) {
+                                mlo[b2] = ml;
+                                mhi[b2] = mh;
+                            }
+                        const uint32_t d = stg0[((used + bsel) % NSLOT) * 32 * STG_PITCH + j] + gg;
+                        key = (d << cb) | (cr + (uint32_t)j);
                     }
                     list_insert<KL>(L, key);
                 }
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sempty[w * NSLOT + slot]);
+                if (lane == 0)
+                    for (int b2 = 0; b2 < nb; ++b2)
+                        tc::mbar_arrive(&sempty[w * NSLOT + (used + b2) % NSLOT]);
+                if (lane == 0) TC_TR(3000 + w * 200 + used, clock64());
+                if (lane == 0) TC_TR(4000 + w * 200 + used, nb * 1000 + R);
                 const uint32_t top = L[KL - 1];
                 const int gd = (top == KEY_INF) ? p.tdr0 : min((int)(top >> cb), p.tdr0);
                 gate_pub[w * 32 + lane] = (uint32_t)(gd + 1);
-                ++used;
+                used += nb;
             }
 
             // ---- output: slot 0 = self, ranks 1.. = list, pads (self, -1); coalesced rows
@@ -511,6 +590,7 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
 
     tc::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TC_TR(1, clock64());
     if (warp == MMA_WARP) {
         tc::tc_fence_after();
         tc::tmem_dealloc<tcm::TMEM_COLS>(tmem);
@@ -519,7 +599,7 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
 
 // Host launcher over the regular grid part of the call.
 template <int S, int KL>
-cudaError_t launch_tc(const MatchParams& p, cudaStream_t stream, int* launches) {
+cudaError_t launch_tc(const MatchParams& p, cudaStream_t stream, int* launches, int only_marked) {
     const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
     if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
     const TcGeom g = TcGeom::make(S, p.r);
@@ -527,7 +607,7 @@ cudaError_t launch_tc(const MatchParams& p, cudaStream_t stream, int* launches) 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.total);
     if (e != cudaSuccess) return e;
     dim3 grid((p.Rx_reg + tcm::TX - 1) / tcm::TX, (kr1 - kr0 + tcm::TY - 1) / tcm::TY, p.B);
-    kern<<<grid, tcm::THREADS, g.total, stream>>>(p);
+    kern<<<grid, tcm::THREADS, g.total, stream>>>(p, only_marked);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

@@ -1,0 +1,30 @@
+"""Dev: run c3 once with a GBM3D_TC_TRACE build and print the timeline of CTA (10,10)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import numpy as np, torch
+import paper_2103_10765_b200 as g
+from synth import CONFIGS, config_images
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]; c = cfg.calls[0]
+img = torch.from_numpy(config_images(cfg)[0]).cuda()
+for _ in range(2):
+    g.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau, check=False, method="product")
+torch.cuda.synchronize()
+lib = g.load_library()
+buf = (ctypes.c_longlong * 8192)()
+lib.gbm3d_dev_tc_trace(buf, 8192)
+t = np.array(buf, dtype=np.int64)
+t0 = t[0]
+print("prologue end -> kernel end:", t[1] - t0)
+mma = t[16:16 + 84] - t0
+print("mma commit issue times:", mma.tolist())
+for w in range(4):
+    tf = t[1000 + 200 * w:1000 + 200 * w + 84] - t0
+    st = t[2000 + 200 * w:2000 + 200 * w + 84]
+    st = np.where(st > 0, st - t0, -1)
+    sel = t[3000 + 200 * w:3000 + 200 * w + 60]
+    sel = np.where(sel > 0, sel - t0, -1)
+    rr = t[4000 + 200 * w:4000 + 200 * w + 60]
+    print(f"w{w} tfull:", tf.tolist())
+    print(f"w{w} staged:", st.tolist())
+    print(f"w{w} selector batches (end time):", sel.tolist())
+    print(f"w{w} selector R:", rr.tolist())
