@@ -126,12 +126,14 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
     bool fast = false;
-    if (method == GBM3D_METHOD_PRODUCT || method == GBM3D_METHOD_PRODUCT_I8) {
+    if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_PRODUCT ||
+        method == GBM3D_METHOD_PRODUCT_I8) {
+        // AUTO prefers the tensor-core product form (fastest where it applies)
         e = tc_dispatch(p, st, &launches, &fast, method == GBM3D_METHOD_PRODUCT_I8);
         if (e != cudaSuccess) return GBM3D_ERR_CUDA;
-        if (!fast) return GBM3D_ERR_UNSUPPORTED;
+        if (!fast && method != GBM3D_METHOD_AUTO) return GBM3D_ERR_UNSUPPORTED;
     }
-    if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_SSD) {
+    if (!fast && (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_SSD)) {
         e = strip_dispatch(p, st, &launches, &fast);
         if (e != cudaSuccess) return GBM3D_ERR_CUDA;
         if (!fast && method == GBM3D_METHOD_SSD) return GBM3D_ERR_UNSUPPORTED;

@@ -33,6 +33,24 @@ def _assert_same(got, exp, what=""):
                         f"got {g_[tuple(bad[0])]} expected {e_[tuple(bad[0])]}")
 
 
+import functools
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle_config(name, ci):
+    cfg = CONFIGS[name]
+    c = cfg.calls[ci]
+    imgs = config_images(cfg)
+    if cfg.B > 1:
+        return oracle.block_match_batched(imgs, c.patch, c.stride, c.radius, c.K, c.tau)
+    return oracle.block_match(imgs[0], c.patch, c.stride, c.radius, c.K, c.tau)
+
+
+def _product_supported(P, s, r, K):
+    """Shapes the tensor-core product kernels take (include/gbm3d.h, GBM3D_METHOD_PRODUCT)."""
+    return P == 8 and s == 3 and 7 * s + 2 * r + 1 <= 64 and 2 <= K <= 32
+
+
 # ----------------------------------------------------------------- the five BASELINE configs
 @pytest.mark.parametrize("name,ci", [("c0", 0), ("c1", 0), ("c1", 1), ("c2", 0)])
 def test_config_parity_small(name, ci):
@@ -43,23 +61,34 @@ def test_config_parity_small(name, ci):
                  oracle.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau), name)
 
 
-def test_config_parity_c3_full():
-    """2048^2, K=32: whole table bit-exact (the bench's launch configuration)."""
+@pytest.mark.parametrize("method", ["auto", "ssd", "product", "product_i8"])
+def test_config_parity_c3_full(method):
+    """2048^2, K=32: whole table bit-exact (auto = the bench's launch configuration)."""
     cfg = CONFIGS["c3"]
     c = cfg.calls[0]
     img = config_images(cfg)[0]
-    _assert_same(_gpu(img, c.patch, c.stride, c.radius, c.K, c.tau),
-                 oracle.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau), "c3")
+    _assert_same(_gpu(img, c.patch, c.stride, c.radius, c.K, c.tau, method=method),
+                 _oracle_config("c3", 0), f"c3 {method}")
 
 
-def test_config_parity_c4_all_images():
-    """Batch of 64 512^2 images in ONE batched launch (the bench's configuration)."""
+@pytest.mark.parametrize("method", ["auto", "ssd", "product", "product_i8"])
+def test_config_parity_c4_all_images(method):
+    """Batch of 64 512^2 images in ONE batched launch (auto = the bench's configuration)."""
     cfg = CONFIGS["c4"]
     c = cfg.calls[0]
     imgs = config_images(cfg)
-    got = _gpu(imgs, c.patch, c.stride, c.radius, c.K, c.tau)
-    exp = oracle.block_match_batched(imgs, c.patch, c.stride, c.radius, c.K, c.tau)
-    _assert_same(got, exp, "c4")
+    got = _gpu(imgs, c.patch, c.stride, c.radius, c.K, c.tau, method=method)
+    _assert_same(got, _oracle_config("c4", 0), f"c4 {method}")
+
+
+@pytest.mark.parametrize("method", ["ssd", "product", "product_i8"])
+@pytest.mark.parametrize("name,ci", [("c0", 0), ("c1", 0), ("c1", 1)])
+def test_config_parity_small_methods(name, ci, method):
+    cfg = CONFIGS[name]
+    c = cfg.calls[ci]
+    img = config_images(cfg)[0]
+    _assert_same(_gpu(img, c.patch, c.stride, c.radius, c.K, c.tau, method=method),
+                 _oracle_config(name, ci), f"{name}/{ci} {method}")
 
 
 # ----------------------------------------------------------------- shapes and edge cases
@@ -96,6 +125,33 @@ def test_edge_cases(H, W, P, s, r, K, tau, kind):
                  f"{kind} {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
 
 
+@pytest.mark.parametrize("method", ["product", "product_i8"])
+@pytest.mark.parametrize("H,W,P,s,r,K,tau,kind",
+                         [e for e in EDGE if _product_supported(e[2], e[3], e[4], e[5])])
+def test_edge_cases_product(H, W, P, s, r, K, tau, kind, method):
+    img = special_image(kind, H, W, seed=H * 1000 + W, lo=-250, hi=500, value=77)
+    _assert_same(_gpu(img, P, s, r, K, tau, method=method), oracle.block_match(img, P, s, r, K, tau),
+                 f"{method} {kind} {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
+
+
+def test_product_mixed_range_tiles():
+    """fp16 tiles next to tiles whose pixel range exceeds the fp16 exactness bound (marked and
+    recomputed by the int8 kernel in the same call)."""
+    rng = np.random.default_rng(7)
+    img = rng.integers(-100, 356, size=(150, 170)).astype(np.int16)
+    img[60:110, 20:90] = rng.choice(np.array([-900, 900], np.int16), size=(50, 70))
+    for K in (16, 32):
+        _assert_same(_gpu(img, 8, 3, 19, K, None, method="product"),
+                     oracle.block_match(img, 8, 3, 19, K, None), f"mixed tiles K{K}")
+
+
+def test_product_unsupported_shape_reports():
+    g = _gbm3d()
+    img = torch.from_numpy(config_images("c2")[0]).cuda()
+    with pytest.raises(g.GBM3DError):
+        g.block_match(img, 12, 4, 19, 16, 720000, method="product")
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_fuzz(seed):
     rng = np.random.default_rng(100 + seed)
@@ -110,19 +166,21 @@ def test_fuzz(seed):
                  f"fuzz {seed}: {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
 
 
-def test_large_distances_exact_fallback():
+@pytest.mark.parametrize("method", ["auto", "ssd", "product_i8"])
+def test_large_distances_exact_fallback(method):
     """Distances above the 32-bit key's d range (2^21-1 at r=19) with no tau: lists fill
     with saturated-range candidates and the in-kernel exact path must take over."""
     img = special_image("uniform", 60, 70, seed=9, lo=-1400, hi=1400)  # E[d] ~ 8e7 >> 2^21
-    _assert_same(_gpu(img, 8, 3, 19, 16, None), oracle.block_match(img, 8, 3, 19, 16, None),
-                 "large distances")
+    _assert_same(_gpu(img, 8, 3, 19, 16, None, method=method),
+                 oracle.block_match(img, 8, 3, 19, 16, None), f"large distances {method}")
 
 
-def test_int16_extremes_within_precondition():
+@pytest.mark.parametrize("method", ["auto", "ssd", "product_i8"])
+def test_int16_extremes_within_precondition(method):
     rng = np.random.default_rng(3)
     img = rng.choice(np.array([-2896, 2896, 0, 1000], np.int16), size=(50, 60))  # 8^2*5792^2 < 2^31
-    _assert_same(_gpu(img, 8, 3, 19, 16, None), oracle.block_match(img, 8, 3, 19, 16, None),
-                 "extremes")
+    _assert_same(_gpu(img, 8, 3, 19, 16, None, method=method),
+                 oracle.block_match(img, 8, 3, 19, 16, None), f"extremes {method}")
 
 
 def test_direct_method_agrees():
