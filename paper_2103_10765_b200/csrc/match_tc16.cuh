@@ -14,11 +14,15 @@
 //     dist slot 0 = TC_TILE_MARK and the exact int8 kernel (match_tc.cuh) redoes such tiles.
 //
 // Work mapping: CTA = 16 x 8 grid references (M = 128, TMEM lane m =
-// reference 8a + b).  Per candidate row: builder warps write the 64 candidate patches (fp16,
-// canonical K-major, 16 B per patch row), one thread issues 4 MMAs (M128 N64 K16) into one of
-// NTS = 8 TMEM stages (64 columns each, one fp32 accumulator), epilogue warp w (lane quarter w)
-// turns its 32 x 64 accumulators into u and a pass mask and stages them; selector warp w keeps
-// the 32 per-lane sorted top-(K-1) register lists (insertion network, one round per pass).
+// reference 8a + b).  The B operand needs no per-row building: the prologue writes the tile's
+// fp16 plane once in a pre-shifted layout X[y][q][m][0..7] = plane[y][8q + m + 0..7] (each
+// 16-byte chunk is candidate column 8q + m's patch row at image row y), so candidate row t's
+// 64 patches are the K-major canonical operand at X + t * 1 KB with LBO = 1 KB (next patch row)
+// and SBO = 128 B (next 8 candidates).  One thread issues 4 MMAs (M128 N64 K16) per candidate
+// row into one of NTS = 8 TMEM stages (64 columns each, one fp32 accumulator); epilogue warp w
+// (lane quarter w) turns its 32 x 64 accumulators into u and a pass mask and stages them;
+// selector warp w keeps the 32 per-lane sorted top-(K-1) register lists (insertion network,
+// one round per pass).
 #pragma once
 #include <cuda_fp16.h>
 
@@ -30,23 +34,28 @@ namespace tc16 {
 constexpr int TY = 16, TX = 8;
 constexpr int NB = 64;           // candidate columns per MMA tile (N)
 constexpr int PCH = 72;          // fp16 plane pitch in elements (64 + 7 + pad)
-constexpr int NSTG = 4;          // B ring stages
 constexpr int NTS = 8;           // TMEM stages (64 columns each)
-constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, BLD_WARP0 = 9, NBLD = 2;
-constexpr int THREADS = 32 * 11;
+#ifndef GBM3D_TC16_NSEL
+#define GBM3D_TC16_NSEL 1
+#endif
+constexpr int NSEL = GBM3D_TC16_NSEL;  // selector warps per lane quarter (rows alternate)
+constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 4 + 4 * NSEL;
+constexpr int THREADS = 32 * (MMA_WARP + 1);
 #ifndef GBM3D_TC16_NSLOT
 #define GBM3D_TC16_NSLOT 2
 #endif
-constexpr int NSLOT = GBM3D_TC16_NSLOT;  // staged rows per epilogue/selector pair
+constexpr int NSLOT = GBM3D_TC16_NSLOT;  // staged rows per lane quarter (a multiple of NSEL)
+static_assert(NSLOT % NSEL == 0, "each selector owns NSLOT / NSEL staging slots");
 constexpr int STG_PITCH = 68;    // words per lane and staged row: u[64], mask lo/hi, gate, row
-constexpr int A_BYTES = 128 * 128, B_BYTES = 64 * 128;
+constexpr int A_BYTES = 128 * 128;
+constexpr int XP = (NB / 8) * 128;  // bytes per pre-shifted plane row (8 chunks of 8 x 16 B)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MMAX = 362;        // exactness bound on max |z - c| (see header)
 }  // namespace tc16
 
 struct Tc16Geom {
     int NT, PR, NJ;
-    int off_a, off_b, off_pl, off_nc, off_stg, off_bar, total;
+    int off_a, off_x, off_nc, off_stg, off_bar, total;
     __host__ __device__ static Tc16Geom make(int S, int r) {
         using namespace tc16;
         Tc16Geom g;
@@ -54,15 +63,14 @@ struct Tc16Geom {
         g.PR = g.NT + 7;
         g.NJ = 7 * S + 2 * r + 1;
         g.off_a = 0;
-        g.off_b = A_BYTES;
-        g.off_pl = g.off_b + NSTG * B_BYTES;
-        g.off_nc = g.off_pl + ((g.PR * PCH * 2 + 15) & ~15);
-        g.off_stg = g.off_nc + g.NT * NB * 4;
+        g.off_x = A_BYTES;                 // pre-shifted plane; horizontal-square scratch before
+        g.off_nc = g.off_x + g.PR * XP;
+        g.off_stg = g.off_nc + g.NT * NB * 4;  // raw int16 tile + fp16 plane before the loop
         g.off_bar = g.off_stg + EPI_WARPS * NSLOT * 32 * STG_PITCH * 4;
-        // full/empty[NSTG], tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT]; gates[128],
-        // consumed[EPI_WARPS], range scratch[2], TMEM address
-        g.total = g.off_bar + (2 * NSTG + 2 * NTS + 2 * EPI_WARPS * NSLOT) * 8 +
-                  (EPI_WARPS * 32 + EPI_WARPS + 2 + 1) * 4 + 16;
+        // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT]; gates[NSEL][128],
+        // consumed[EPI_WARPS][NSEL], range scratch[2], TMEM address
+        g.total = g.off_bar + (2 * NTS + 2 * EPI_WARPS * NSLOT) * 8 +
+                  (NSEL * EPI_WARPS * 32 + EPI_WARPS * NSEL + 2 + 1) * 4 + 16;
         return g;
     }
 };
@@ -118,6 +126,7 @@ template <int S, int KL>
 __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParams p) {
     using namespace tc16;
     extern __shared__ __align__(1024) unsigned char sm[];
+    if (threadIdx.x == 0) TC_TR(2, clock64());
     const Tc16Geom g = Tc16Geom::make(S, p.r);
     constexpr int P = 8;
     const int r = p.r;
@@ -128,18 +137,19 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     const int gy0 = S * ky0 - r, gx0 = S * kx0 - r;
     const int16_t* __restrict__ img = p.img + (int64_t)bimg * p.img_bstride;
 
-    __half* const pl = reinterpret_cast<__half*>(sm + g.off_pl);
+    // raw int16 tile and the fp16 plane live in the (not yet used) staging area
+    int16_t* const raw = reinterpret_cast<int16_t*>(sm + g.off_stg);
+    __half* const pl = reinterpret_cast<__half*>(sm + g.off_stg + ((g.PR * PCH * 2 + 15) & ~15));
     float* const nc = reinterpret_cast<float*>(sm + g.off_nc);
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
-    uint64_t* const full = bars;
-    uint64_t* const empty = bars + NSTG;
-    uint64_t* const tfull = bars + 2 * NSTG;
+    uint64_t* const tfull = bars;
     uint64_t* const tempty = tfull + NTS;
     uint64_t* const sfull = tempty + NTS;
     uint64_t* const sempty = sfull + EPI_WARPS * NSLOT;
     volatile int* const gate_pub = reinterpret_cast<volatile int*>(sempty + EPI_WARPS * NSLOT);
-    volatile int* const consumed = gate_pub + EPI_WARPS * 32;  // staged rows taken by selector w
-    int* const rng = const_cast<int*>(consumed + EPI_WARPS);   // tile min, max
+    // rows taken by selector (w, h)
+    volatile int* const consumed = gate_pub + NSEL * EPI_WARPS * 32;
+    int* const rng = const_cast<int*>(consumed + EPI_WARPS * NSEL);  // tile min, max
     uint32_t* const tslot = reinterpret_cast<uint32_t*>(rng + 2);
 
     const int t_lo = max(0, -gy0), t_hi = min(g.NT - 1, (p.H - P) - gy0);
@@ -147,7 +157,6 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     const int nseq = t_hi - t_lo + 1;
 
     // ---- prologue: raw pixels (int16 scratch in the staging area) and the tile range
-    int16_t* const raw = reinterpret_cast<int16_t*>(sm + g.off_stg);
     {
         if (threadIdx.x == 0) {
             rng[0] = INT_MAX;
@@ -178,6 +187,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             atomicMax(&rng[1], hi);
         }
         __syncthreads();
+        if (threadIdx.x == 0) TC_TR(3, clock64());
     }
     const int zlo = rng[0], zhi = rng[1];
     const int cz = (zlo + zhi) >> 1;
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     }
     {
         // centred fp16 plane, squares -> horizontal sums (scratch in the B ring) -> norms
-        int* const hs = reinterpret_cast<int*>(sm + g.off_b);
+        int* const hs = reinterpret_cast<int*>(sm + g.off_x);
         const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
         // pixels outside the image only feed masked candidates: store them as 0 (= c)
         for (int i = threadIdx.x; i < g.PR * PCH; i += THREADS) {
@@ -202,10 +212,6 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             pl[i] = __int2half_rn(v);
         }
         if (threadIdx.x == 0) {
-            for (int i = 0; i < NSTG; ++i) {
-                tc::mbar_init(&full[i], NBLD);
-                tc::mbar_init(&empty[i], 1);
-            }
             for (int i = 0; i < NTS; ++i) {
                 tc::mbar_init(&tfull[i], 1);
                 tc::mbar_init(&tempty[i], EPI_WARPS);
@@ -217,9 +223,10 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             tc::fence_mbar_init();
         }
         if (warp == MMA_WARP) tc::tmem_alloc<TMEM_COLS>(tslot);
-        if (threadIdx.x < EPI_WARPS * 32) gate_pub[threadIdx.x] = p.tdr0 + 1;
-        if (threadIdx.x < EPI_WARPS) consumed[threadIdx.x] = 0;
+        if (threadIdx.x < NSEL * EPI_WARPS * 32) gate_pub[threadIdx.x] = p.tdr0 + 1;
+        if (threadIdx.x < EPI_WARPS * NSEL) consumed[threadIdx.x] = 0;
         __syncthreads();  // centred raw values complete
+        if (threadIdx.x == 0) TC_TR(4, clock64());
         for (int i = threadIdx.x; i < g.PR * NB; i += THREADS) {
             const int row = i >> 6, c = i & 63;
             const int16_t* q = raw + row * PCH + c;
@@ -236,6 +243,14 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             for (int k = 0; k < P; ++k) s += q[k * NB];
             nc[i] = (float)s;  // <= 64 M^2 < 2^24: exact
         }
+        __syncthreads();  // horizontal squares consumed: the plane area is free
+        if (threadIdx.x == 0) TC_TR(5, clock64());
+        uint8_t* const xop = sm + g.off_x;
+        for (int u = threadIdx.x; u < g.PR * NB; u += THREADS) {
+            const int y = u >> 6, n = u & 63;
+            *reinterpret_cast<uint4*>(xop + y * XP + (n >> 3) * 128 + (n & 7) * 16) =
+                load16h(pl + y * PCH, n);
+        }
         uint8_t* const a_op = sm + g.off_a;
         for (int u = threadIdx.x; u < 128 * P; u += THREADS) {
             const int m = u >> 3, i = u & 7;
@@ -250,37 +265,23 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     const uint32_t tmem = *tslot;
     if (threadIdx.x == 0) TC_TR(0, clock64());
 
-    if (warp >= BLD_WARP0) {
-        const int n = threadIdx.x - 32 * BLD_WARP0;
-        RowSeq seq;
-        seq.init(S, r, t_lo, t_hi);
-        for (int s = 0; s < nseq; ++s) {
-            const int stage = s % NSTG;
-            if (s >= NSTG) tc::mbar_wait(&empty[stage], ((s / NSTG) - 1) & 1);
-            const int t = seq.next();
-            uint8_t* const bop = sm + g.off_b + stage * B_BYTES;
-#pragma unroll
-            for (int i = 0; i < P; ++i)
-                *reinterpret_cast<uint4*>(bop + kmaj16_off(n, i)) = load16h(pl + (t + i) * PCH, n);
-            tc::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&full[stage]);
-        }
-    } else if (warp == MMA_WARP) {
+    if (warp == MMA_WARP) {
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_f16f16_f32(128, NB);
             const uint32_t aa = tc::smem_u32(sm + g.off_a);
+            const uint32_t xa = tc::smem_u32(sm + g.off_x);
+            RowSeq seq;
+            seq.init(S, r, t_lo, t_hi);
             for (int s = 0; s < nseq; ++s) {
-                const int stage = s % NSTG, ts = s % NTS;
-                tc::mbar_wait(&full[stage], (s / NSTG) & 1);
+                const int ts = s % NTS;
+                const int t = seq.next();
                 if (s >= NTS) tc::mbar_wait(&tempty[ts], ((s / NTS) - 1) & 1);
                 tc::tc_fence_after();
-                const uint32_t bb = tc::smem_u32(sm + g.off_b + stage * B_BYTES);
+                const uint32_t bb = xa + (uint32_t)(t * XP);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
                     tc::mma_f16(tmem + (uint32_t)(ts * NB), tc::smem_desc(aa + ks * 256, 128, 1024),
-                                tc::smem_desc(bb + ks * 256, 128, 1024), idesc, ks);
-                tc::mma_commit(&empty[stage]);
+                                tc::smem_desc(bb + ks * 2 * XP, XP, 128), idesc, ks);
                 tc::mma_commit(&tfull[ts]);
                 TC_TR(16 + s, clock64());
             }
@@ -288,7 +289,8 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
         __syncwarp();
     } else {
         const bool is_sel = warp >= SEL_WARP0;
-        const int w = is_sel ? warp - SEL_WARP0 : warp;
+        const int w = is_sel ? (warp - SEL_WARP0) & 3 : warp;
+        const int hsel = is_sel ? (warp - SEL_WARP0) >> 2 : 0;  // this selector's row parity
         const int a = 4 * w + (lane >> 3), bb = lane & 7;
         const bool refok = (ky0 + a < kr1) && (kx0 + bb < p.Rx_reg) && (p.K > 1);
         const int ty = r + S * a, tx = r + S * bb;
@@ -323,40 +325,58 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 if (used >= NSLOT) tc::mbar_wait(&sempty[w * NSLOT + slot], ((used / NSLOT) - 1) & 1);
                 // while the lists fill (gates still at their start value) stage one row at a
                 // time: a row staged against an unset gate passes its whole window
-                int gate = gate_pub[w * 32 + lane];
+                // (the selectors' lists each hold K-1 keys below their own top, so the smallest
+                // published top bounds the final (K-1)-th key: every selector may gate with it)
+                auto read_gate = [&]() {
+                    int gt = gate_pub[w * 32 + lane];
+#pragma unroll
+                    for (int h = 1; h < NSEL; ++h) gt = min(gt, gate_pub[h * EPI_WARPS * 32 + w * 32 + lane]);
+                    return gt;
+                };
+                int gate = read_gate();
                 if (used > 0 && __any_sync(0xffffffffu, gate == gate0 && refok)) {
-                    while (consumed[w] < used) {
+                    for (;;) {
+                        int c = 0;
+#pragma unroll
+                        for (int h = 0; h < NSEL; ++h) c += consumed[w * NSEL + h];
+                        if (c >= used) break;
                     }
-                    gate = gate_pub[w * 32 + lane];
+                    gate = read_gate();
                 }
-                const float T = (float)(gate - __float2int_rn(Nr));  // pass iff u < T
+                // u = N_q - 2 <f_p, f_q> passes iff u < T = gate - N_p; stage v = u - T (exact for
+                // every passing candidate, sign-correct for the rest): d = v + gate
+                const float T = (float)(gate - __float2int_rn(Nr));
                 uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                 tc::tc_fence_after();
                 uint32_t msk[2] = {0u, 0u};
                 const uint32_t tb = taddr + (uint32_t)(ts * NB);
+                uint32_t acc[64];
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t acc[16];
-                    tc::tmem_ld16(tb + ch * 16, acc);
-                    tc::tmem_wait_ld(acc);
+                for (int ch = 0; ch < 4; ++ch) tc::tmem_ld16p(tb + ch * 16, acc + ch * 16);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) tc::tmem_tie16(acc + ch * 16);
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int ch = cc ^ 1;  // per 32-column half, the upper 16 columns first
                     const float4* ncv = reinterpret_cast<const float4*>(nc + t * NB + ch * 16);
-                    float u[16];
+                    float v[16];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const float4 n4 = ncv[q];
-                        u[4 * q + 0] = fmaf(__uint_as_float(acc[4 * q + 0]), -2.f, n4.x);
-                        u[4 * q + 1] = fmaf(__uint_as_float(acc[4 * q + 1]), -2.f, n4.y);
-                        u[4 * q + 2] = fmaf(__uint_as_float(acc[4 * q + 2]), -2.f, n4.z);
-                        u[4 * q + 3] = fmaf(__uint_as_float(acc[4 * q + 3]), -2.f, n4.w);
+                        v[4 * q + 0] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 0]), -2.f, n4.x - T);
+                        v[4 * q + 1] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 1]), -2.f, n4.y - T);
+                        v[4 * q + 2] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 2]), -2.f, n4.z - T);
+                        v[4 * q + 3] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 3]), -2.f, n4.w - T);
                     }
-                    uint32_t m = 0;
+                    // shift the sign bits in, highest column first: bit j of msk = column j passes
+                    uint32_t& m = msk[ch >> 1];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) m |= (u[j] < T ? 1u : 0u) << j;
-                    msk[ch >> 1] |= m << ((ch & 1) * 16);
+                    for (int j = 15; j >= 0; --j) m = __funnelshift_l(__float_as_uint(v[j]), m, 1);
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         *reinterpret_cast<float4*>(stg + ch * 16 + 4 * q) =
-                            make_float4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+                            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                 }
                 tc::tc_fence_before();
                 __syncwarp();
@@ -382,15 +402,15 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 nrel = hi >= lo ? hi - lo + 1 : 0;
             }
             // d + 2^23 as an fp32 bit pattern is 0x4B000000 + d (exact for d < 2^23), and
-            // 0x4B000000 << cb == 0 (mod 2^32) for cb >= 8: key = bits(u + N_p + 2^23) << cb | code
-            const float NrB = Nr + 8388608.0f;
+            // 0x4B000000 << cb == 0 (mod 2^32) for cb >= 8: key = bits(v + gate + 2^23) << cb | code
             const uint32_t kmul = 1u << cb;
-            for (; used < nrel; ++used) {
+            for (used = hsel; used < nrel; used += NSEL) {
                 const int slot = used % NSLOT;
                 tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
                 const uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                 const uint4 hdr = *reinterpret_cast<const uint4*>(stg + 64);
                 uint32_t mlo = hdr.x, mhi = hdr.y;
+                const float GB = (float)(int)hdr.z + 8388608.0f;  // d + 2^23 = v + gate + 2^23
                 const uint32_t code_row = (uint32_t)((int)hdr.w - S * a) * side - (uint32_t)(S * bb);
                 const int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
                 // next pending candidate (highest column first), software-pipelined one round
@@ -402,7 +422,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                     const int j = (hi ? 32 : 0) + max(jb, 0);
                     const uint32_t clr = m ^ (jb >= 0 ? (1u << jb) : 0u);
                     if (hi) mhi = clr; else mlo = clr;
-                    const uint32_t bits = __float_as_uint(__uint_as_float(stg[j]) + NrB);
+                    const uint32_t bits = __float_as_uint(__uint_as_float(stg[j]) + GB);
                     return jb >= 0 ? bits * kmul + code_row + (uint32_t)j : KEY_INF;
                 };
                 uint32_t key = next_key();
@@ -416,51 +436,129 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 if (lane == 0) TC_TR(3000 + w * 200 + used, clock64());
                 if (lane == 0) TC_TR(4000 + w * 200 + used, R);
                 const uint32_t top = L[KL - 1];
-                gate_pub[w * 32 + lane] = ((top == KEY_INF) ? p.tdr0 : min((int)(top >> cb), p.tdr0)) + 1;
+                gate_pub[hsel * EPI_WARPS * 32 + w * 32 + lane] =
+                    ((top == KEY_INF) ? p.tdr0 : min((int)(top >> cb), p.tdr0)) + 1;
                 __syncwarp();
-                if (lane == 0) consumed[w] = used + 1;
+                if (lane == 0) consumed[w * NSEL + hsel] = used / NSEL + 1;
+            }
+            if constexpr (NSEL > 1) {
+                // merge: selector h > 0 leaves its sorted list in its last staging slot (all rows
+                // consumed), selector 0 inserts the keys below its own top
+                uint32_t* const mine = stg0 + (NSLOT - NSEL + hsel) * 32 * STG_PITCH;
+                if (hsel > 0) {
+#pragma unroll
+                    for (int i = 0; i < KL; ++i) mine[i] = L[i];
+                }
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + w), "r"(32 * NSEL) : "memory");
+#pragma unroll 1
+                for (int h = 1; hsel == 0 && h < NSEL; ++h) {
+                    const uint32_t* const other = stg0 + (NSLOT - NSEL + h) * 32 * STG_PITCH;
+#pragma unroll 1
+                    for (int i = 0; i < KL; ++i) {
+                        const uint32_t x = other[i];
+                        if (!__any_sync(0xffffffffu, x < L[KL - 1])) break;
+                        list_insert<KL>(L, x);
+                    }
+                }
+                __syncwarp();
             }
 
+            if (hsel == 0) {
+            if (threadIdx.x == 32 * SEL_WARP0) TC_TR(7, clock64());
             // ---- output: slot 0 = self, ranks 1.. = list, pads (self, -1); coalesced rows
-            uint32_t* const stg = stg0;
             const int Kout = p.K;
             const int ry = S * (ky0 + a), rx = S * (kx0 + bb);
             const int self = ry * p.W + rx;
             const uint32_t cmask = (1u << cb) - 1u;
+            // idx = self + dy W + dx with code = (dy + r) side + (dx + r): with q = code / side
+            // (exact through the fp32 reciprocal: code < 2^13, side <= 65),
+            // idx = self - r (W + 1) + code + q (W - side)
+            const float inv_side = 1.0f / (float)side;
+            const int ibase = self - r * (p.W + 1), wms = p.W - (int)side;
             int cnt = 0;
-            __syncwarp();
-            stg[0] = (uint32_t)self;
-            stg[Kout] = 0u;
-#pragma unroll
-            for (int i = 0; i < KL; ++i) {
-                if (i + 1 < Kout) {
-                    const uint32_t key = L[i];
-                    int32_t vi = self, vd = -1;
+            const int64_t ref0 = (int64_t)bimg * p.out_bstride;
+            // per-warp output block: idx [4 rows][8 refs][Kout], then dist likewise
+            uint32_t* const ob = reinterpret_cast<uint32_t*>(sm + g.off_stg) + w * NSLOT * 32 * STG_PITCH;
+            auto slot_val = [&](int i, int32_t& vi, int32_t& vd) {  // i = slot (static)
+                vi = self;
+                vd = i == 0 ? 0 : -1;
+                if (i > 0) {
+                    const uint32_t key = L[i - 1];
                     if (key != KEY_INF) {
                         const uint32_t code = key & cmask;
-                        const int dy = (int)(code / side) - r, dx = (int)(code % side) - r;
-                        vi = (ry + dy) * p.W + rx + dx;
+                        const int q = (int)(((float)code + 0.5f) * inv_side);
+                        vi = ibase + (int)code + q * wms;
                         vd = (int32_t)(key >> cb);
-                        ++cnt;
                     }
-                    stg[1 + i] = (uint32_t)vi;
-                    stg[Kout + 1 + i] = (uint32_t)vd;
+                }
+            };
+#pragma unroll
+            for (int i = 0; i < KL; ++i) cnt += (i + 1 < Kout && L[i] != KEY_INF) ? 1 : 0;
+            __syncwarp();
+            const int nref = min(8, p.Rx_reg - kx0);
+            if ((Kout & 3) == 0) {
+                // 16-byte chunks c of a reference row stored at chunk c ^ (b & swz): conflict-free
+                // stores (lanes b = 0..7 of a phase hit distinct banks) and contiguous reads
+                const int nch = Kout >> 2;
+                const int swz = (nch & (nch - 1)) == 0 ? nch - 1 : 0;
+                uint32_t* const oi = ob + (lane >> 3) * 8 * Kout + bb * Kout;
+                uint32_t* const od = oi + 32 * Kout;
+#pragma unroll
+                for (int c = 0; c < (KL + 1) / 4; ++c) {
+                    if (4 * c < Kout) {
+                        int32_t i0, i1, i2, i3, d0, d1, d2, d3;
+                        slot_val(4 * c + 0, i0, d0);
+                        slot_val(4 * c + 1, i1, d1);
+                        slot_val(4 * c + 2, i2, d2);
+                        slot_val(4 * c + 3, i3, d3);
+                        const int cs = (c ^ (bb & swz)) * 4;
+                        *reinterpret_cast<int4*>(oi + cs) = make_int4(i0, i1, i2, i3);
+                        *reinterpret_cast<int4*>(od + cs) = make_int4(d0, d1, d2, d3);
+                    }
+                }
+                __syncwarp();
+                if (threadIdx.x == 32 * SEL_WARP0) TC_TR(8, clock64());
+                const int n16 = nref * nch;
+#pragma unroll
+                for (int al = 0; al < 4; ++al) {
+                    if (ky0 + 4 * w + al >= kr1) break;
+                    const int64_t row = ref0 + (int64_t)(ky0 + 4 * w + al - p.row_begin) * p.Rx + kx0;
+                    int4* const gi = reinterpret_cast<int4*>(p.idx + row * Kout);
+                    int4* const gd = reinterpret_cast<int4*>(p.dist + row * Kout);
+                    const uint32_t* const si = ob + al * 8 * Kout;
+                    for (int u = lane; u < n16; u += 32) {
+                        const int b2 = u / nch, c = u - b2 * nch;
+                        const int off = b2 * Kout + ((c ^ (b2 & swz)) << 2);
+                        gi[u] = *reinterpret_cast<const int4*>(si + off);
+                        gd[u] = *reinterpret_cast<const int4*>(si + 32 * Kout + off);
+                    }
+                }
+            } else {
+                // general K: one word per slot, each reference row written by the warp
+                uint32_t* const oi = ob + lane * Kout;
+                uint32_t* const od = oi + 32 * Kout;
+#pragma unroll
+                for (int i = 0; i < KL + 1; ++i) {
+                    if (i < Kout) {
+                        int32_t vi, vd;
+                        slot_val(i, vi, vd);
+                        oi[i] = (uint32_t)vi;
+                        od[i] = (uint32_t)vd;
+                    }
+                }
+                __syncwarp();
+                for (int l = 0; l < 32; ++l) {
+                    const int la = 4 * w + (l >> 3), lb = l & 7;
+                    if (ky0 + la >= kr1 || lb >= nref) continue;
+                    const int64_t ref = ref0 + (int64_t)(ky0 + la - p.row_begin) * p.Rx + (kx0 + lb);
+                    for (int s2 = lane; s2 < Kout; s2 += 32) {
+                        p.idx[ref * Kout + s2] = (int32_t)ob[l * Kout + s2];
+                        p.dist[ref * Kout + s2] = (int32_t)ob[32 * Kout + l * Kout + s2];
+                    }
                 }
             }
             __syncwarp();
-            const int64_t ref0 = (int64_t)bimg * p.out_bstride;
-            for (int l = 0; l < 32; ++l) {
-                const int la = 4 * w + (l >> 3), lb = l & 7;
-                if (ky0 + la >= kr1 || kx0 + lb >= p.Rx_reg) continue;
-                const int64_t ref = ref0 + (int64_t)(ky0 + la - p.row_begin) * p.Rx + (kx0 + lb);
-                const uint32_t* src = reinterpret_cast<uint32_t*>(sm + g.off_stg) +
-                                      (w * NSLOT * 32 + l) * STG_PITCH;
-                for (int s2 = lane; s2 < Kout; s2 += 32) {
-                    p.idx[ref * Kout + s2] = (int32_t)src[s2];
-                    p.dist[ref * Kout + s2] = (int32_t)src[Kout + s2];
-                }
-            }
-            __syncwarp();
+            if (threadIdx.x == 32 * SEL_WARP0) TC_TR(9, clock64());
             if (refok && p.tau_above_dsat && cnt < Kout - 1) {
                 const int wy = min(p.H - P, ry + r) - max(0, ry - r) + 1;
                 const int wx = min(p.W - P, rx + r) - max(0, rx - r) + 1;
@@ -474,6 +572,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             if (refok && p.nvalid) {
                 const int64_t ref = ref0 + (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
                 p.nvalid[ref] = 1 + cnt;
+            }
             }
         }
     }
@@ -492,6 +591,7 @@ cudaError_t launch_tc16(const MatchParams& p, cudaStream_t stream, int* launches
     const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
     if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
     const Tc16Geom g = Tc16Geom::make(S, p.r);
+    static_assert(tc16::NB == 64, "pre-shifted plane layout assumes 64 candidate columns");
     auto kern = match_tc16_kernel<S, KL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.total);
     if (e != cudaSuccess) return e;

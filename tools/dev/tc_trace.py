@@ -5,16 +5,20 @@ import numpy as np, torch
 import paper_2103_10765_b200 as g
 from synth import CONFIGS, config_images
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]; c = cfg.calls[0]
+K = int(sys.argv[2]) if len(sys.argv) > 2 else c.K
+tau = (None if sys.argv[3] == "none" else int(sys.argv[3])) if len(sys.argv) > 3 else c.tau
 img = torch.from_numpy(config_images(cfg)[0]).cuda()
 for _ in range(2):
-    g.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau, check=False, method="product")
+    g.block_match(img, c.patch, c.stride, c.radius, K, tau, check=False, method="product")
 torch.cuda.synchronize()
 lib = g.load_library()
 buf = (ctypes.c_longlong * 8192)()
 lib.gbm3d_dev_tc_trace(buf, 8192)
 t = np.array(buf, dtype=np.int64)
 t0 = t[0]
-print("prologue end -> kernel end:", t[1] - t0)
+print("kernel start -> prologue end:", t0 - t[2], " prologue end -> kernel end:", t[1] - t0)
+print("prologue marks from start (raw, plane, nc, loop):", [int(t[i] - t[2]) for i in (3, 4, 5, 0)])
+print("output marks from loop start (out start, staged, stored, end):", [int(t[i] - t0) for i in (7, 8, 9, 1)])
 mma = t[16:16 + 84] - t0
 print("mma commit issue times:", mma.tolist())
 for w in range(4):

@@ -1,5 +1,5 @@
 """Per-CUDA-source-line totals (stall samples, warp instructions) from an ncu report.
-Usage: python tools/ncu_lines.py report.ncu-rep [topN]"""
+Usage: python tools/ncu_lines.py report.ncu-rep [topN] [function-substring]"""
 import collections
 import csv
 import io
@@ -8,6 +8,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+want = sys.argv[3] if len(sys.argv) > 3 else None
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -16,7 +17,13 @@ ins = collections.Counter()
 text = {}
 fname = ""
 hdr = None
+func = ""
 for r in rows:
+    if r and r[0] == "Function Name":
+        func = r[1]
+        continue
+    if want and want not in func:
+        continue
     if r and r[0] == "File Path":
         fname = r[1].split("/")[-1]
         continue
