@@ -51,6 +51,10 @@ constexpr int A_BYTES = 128 * 128;
 constexpr int XP = (NB / 8) * 128;  // bytes per pre-shifted plane row (8 chunks of 8 x 16 B)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MMAX = 362;        // exactness bound on max |z - c| (see header)
+#ifndef GBM3D_TC16_BULK_MIN
+#define GBM3D_TC16_BULK_MIN 16
+#endif
+constexpr int BULK_MIN = GBM3D_TC16_BULK_MIN;  // rows with this many passes (max over lanes) merge in bulk
 }  // namespace tc16
 
 struct Tc16Geom {
@@ -63,9 +67,9 @@ struct Tc16Geom {
         g.PR = g.NT + 7;
         g.NJ = 7 * S + 2 * r + 1;
         g.off_a = 0;
-        g.off_x = A_BYTES;                 // pre-shifted plane; horizontal-square scratch before
+        g.off_x = A_BYTES;                 // pre-shifted plane
         g.off_nc = g.off_x + g.PR * XP;
-        g.off_stg = g.off_nc + g.NT * NB * 4;  // raw int16 tile + fp16 plane before the loop
+        g.off_stg = g.off_nc + g.NT * NB * 4;  // raw tile, fp16 plane, squares before the loop
         g.off_bar = g.off_stg + EPI_WARPS * NSLOT * 32 * STG_PITCH * 4;
         // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT]; gates[NSEL][128],
         // consumed[EPI_WARPS][NSEL], range scratch[2], TMEM address
@@ -74,6 +78,47 @@ struct Tc16Geom {
         return g;
     }
 };
+
+// Ascending bitonic sort of N (power of two) register keys; fully unrolled min/max network.
+template <int N>
+static __device__ __forceinline__ void bitonic_sort(uint32_t (&B)[N]) {
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const uint32_t lo = min(B[i], B[l]), hi = max(B[i], B[l]);
+                    const bool asc = (i & k) == 0;
+                    B[i] = asc ? lo : hi;
+                    B[l] = asc ? hi : lo;
+                }
+            }
+        }
+    }
+}
+// L (ascending, N keys) <- the N smallest of L and B (any order): sort B, take the lower half
+// of the bitonic sequence L ++ reverse(B) (min(L[i], B[N-1-i])), then one bitonic clean-up.
+template <int N>
+static __device__ __forceinline__ void bulk_merge(uint32_t (&L)[N], uint32_t (&B)[N]) {
+    bitonic_sort<N>(B);
+#pragma unroll
+    for (int i = 0; i < N; ++i) L[i] = min(L[i], B[N - 1 - i]);
+#pragma unroll
+    for (int j = N >> 1; j > 0; j >>= 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const int l = i ^ j;
+            if (l > i) {
+                const uint32_t lo = min(L[i], L[l]), hi = max(L[i], L[l]);
+                L[i] = lo;
+                L[l] = hi;
+            }
+        }
+    }
+}
 
 // 8 consecutive fp16 (16 bytes) starting at element c of a 4-byte aligned shared row.
 static __device__ __forceinline__ uint4 load16h(const __half* row, int c) {
@@ -139,7 +184,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
 
     // raw int16 tile and the fp16 plane live in the (not yet used) staging area
     int16_t* const raw = reinterpret_cast<int16_t*>(sm + g.off_stg);
-    __half* const pl = reinterpret_cast<__half*>(sm + g.off_stg + ((g.PR * PCH * 2 + 15) & ~15));
+    __half* const pl = reinterpret_cast<__half*>(sm + g.off_stg + g.PR * PCH * 2);
     float* const nc = reinterpret_cast<float*>(sm + g.off_nc);
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
     uint64_t* const tfull = bars;
@@ -156,25 +201,48 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     const int j_lo = max(0, -gx0), j_hi = min(g.NJ - 1, (p.W - P) - gx0);
     const int nseq = t_hi - t_lo + 1;
 
-    // ---- prologue: raw pixels (int16 scratch in the staging area) and the tile range
+    // ---- prologue.  Work items are (row, 8-column segment) of the PR x 72 pixel tile: raw
+    // int16 (pitch 144 B), the centred fp16 plane, the horizontal squares and the norms all live
+    // in the staging area, which the main loop only uses afterwards.
+    constexpr int SEG = PCH / 8;                                // 9 segments of 8 columns
+    constexpr int NIT = (95 * SEG + THREADS - 1) / THREADS;     // PR <= 95 (radius <= 21)
+    int* const hs = reinterpret_cast<int*>(sm + g.off_stg + 2 * g.PR * PCH * 2);
+    const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
     {
         if (threadIdx.x == 0) {
             rng[0] = INT_MAX;
             rng[1] = INT_MIN;
         }
         __syncthreads();
-        const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
         int lo = INT_MAX, hi = INT_MIN;
-        for (int i = threadIdx.x; i < g.PR * PCH; i += THREADS) {
-            const int row = i / PCH, col = i - row * PCH;
-            const int gy = gy0 + row, gx = gx0 + col;
-            const bool in = gy >= ylo && gy < yhi && gx >= 0 && gx < p.W;
-            const int z = in ? (int)img[(int64_t)(gy - p.slab_y0) * p.W + gx] : 0;
-            raw[i] = (int16_t)z;
-            // only pixels that can be part of a valid candidate patch count for the range
-            if (in && gy <= p.H - 1 && gx <= p.W - 1) {
-                lo = min(lo, z);
-                hi = max(hi, z);
+        int16_t z[NIT][8];
+#pragma unroll
+        for (int k = 0; k < NIT; ++k) {  // all loads of a thread in flight together
+            const int task = threadIdx.x + k * THREADS;
+            const int row = task / SEG, seg = task - row * SEG;
+            const int gy = gy0 + row, gx = gx0 + 8 * seg;
+            const bool rowok = task < g.PR * SEG && gy >= ylo && gy < yhi;
+            const int16_t* src = img + (int64_t)(gy - p.slab_y0) * p.W;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const bool in = rowok && gx + j >= 0 && gx + j < p.W;
+                z[k][j] = in ? src[gx + j] : (int16_t)0;
+                if (in) {
+                    lo = min(lo, (int)z[k][j]);
+                    hi = max(hi, (int)z[k][j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NIT; ++k) {
+            const int task = threadIdx.x + k * THREADS;
+            if (task < g.PR * SEG) {
+                uint4 v;
+                v.x = (uint32_t)(uint16_t)z[k][0] | ((uint32_t)(uint16_t)z[k][1] << 16);
+                v.y = (uint32_t)(uint16_t)z[k][2] | ((uint32_t)(uint16_t)z[k][3] << 16);
+                v.z = (uint32_t)(uint16_t)z[k][4] | ((uint32_t)(uint16_t)z[k][5] << 16);
+                v.w = (uint32_t)(uint16_t)z[k][6] | ((uint32_t)(uint16_t)z[k][7] << 16);
+                *reinterpret_cast<uint4*>(raw + task * 8) = v;  // row * PCH + 8 seg == 8 task
             }
         }
 #pragma unroll
@@ -199,17 +267,27 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
         return;
     }
     {
-        // centred fp16 plane, squares -> horizontal sums (scratch in the B ring) -> norms
-        int* const hs = reinterpret_cast<int*>(sm + g.off_x);
-        const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
-        // pixels outside the image only feed masked candidates: store them as 0 (= c)
-        for (int i = threadIdx.x; i < g.PR * PCH; i += THREADS) {
-            const int row = i / PCH, col = i - row * PCH;
-            const int gy = gy0 + row, gx = gx0 + col;
-            const bool in = gy >= ylo && gy < yhi && gx >= 0 && gx < p.W;
-            const int v = in ? raw[i] - cz : 0;
-            raw[i] = (int16_t)v;
-            pl[i] = __int2half_rn(v);
+        // centre on cz; pixels outside the image only feed masked candidates: 0 (= cz)
+        for (int task = threadIdx.x; task < g.PR * SEG; task += THREADS) {
+            const int row = task / SEG, seg = task - row * SEG;
+            const int gy = gy0 + row, gx = gx0 + 8 * seg;
+            const bool rowok = gy >= ylo && gy < yhi;
+            const uint4 rv = *reinterpret_cast<const uint4*>(raw + task * 8);
+            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+            uint32_t iw[4], hw[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 2 * q;
+                const bool in0 = rowok && gx + j >= 0 && gx + j < p.W;
+                const bool in1 = rowok && gx + j + 1 >= 0 && gx + j + 1 < p.W;
+                const int v0 = in0 ? (int)(int16_t)(rw[q] & 0xffffu) - cz : 0;
+                const int v1 = in1 ? (int)(int16_t)(rw[q] >> 16) - cz : 0;
+                iw[q] = (uint32_t)(uint16_t)v0 | ((uint32_t)(uint16_t)v1 << 16);
+                const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
+                hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(raw + task * 8) = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+            *reinterpret_cast<uint4*>(pl + task * 8) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         }
         if (threadIdx.x == 0) {
             for (int i = 0; i < NTS; ++i) {
@@ -225,37 +303,65 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
         if (warp == MMA_WARP) tc::tmem_alloc<TMEM_COLS>(tslot);
         if (threadIdx.x < NSEL * EPI_WARPS * 32) gate_pub[threadIdx.x] = p.tdr0 + 1;
         if (threadIdx.x < EPI_WARPS * NSEL) consumed[threadIdx.x] = 0;
-        __syncthreads();  // centred raw values complete
+        __syncthreads();  // centred raw values and the fp16 plane complete
         if (threadIdx.x == 0) TC_TR(4, clock64());
-        for (int i = threadIdx.x; i < g.PR * NB; i += THREADS) {
-            const int row = i >> 6, c = i & 63;
-            const int16_t* q = raw + row * PCH + c;
-            int s = 0;
+        // horizontal P-sums of squares hs[y][n] (n < 64), 8 columns per item (sliding sum)
+        for (int task = threadIdx.x; task < g.PR * 8; task += THREADS) {
+            const int y = task >> 3, k = task & 7;
+            const uint4 r0 = *reinterpret_cast<const uint4*>(raw + y * PCH + 8 * k);
+            const uint4 r1 = *reinterpret_cast<const uint4*>(raw + y * PCH + 8 * k + 8);
+            const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            int sq[16];
 #pragma unroll
-            for (int j = 0; j < P; ++j) s += (int)q[j] * (int)q[j];
-            hs[i] = s;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < g.NT * NB; i += THREADS) {
-            const int* q = hs + i;
-            int s = 0;
+            for (int q = 0; q < 8; ++q) {
+                const int a0 = (int)(int16_t)(rw[q] & 0xffffu), a1 = (int)(int16_t)(rw[q] >> 16);
+                sq[2 * q] = a0 * a0;
+                sq[2 * q + 1] = a1 * a1;
+            }
+            int o[8];
+            int sacc = 0;
 #pragma unroll
-            for (int k = 0; k < P; ++k) s += q[k * NB];
-            nc[i] = (float)s;  // <= 64 M^2 < 2^24: exact
+            for (int j = 0; j < P; ++j) sacc += sq[j];
+            o[0] = sacc;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                sacc += sq[i + P - 1] - sq[i - 1];
+                o[i] = sacc;
+            }
+            *reinterpret_cast<int4*>(hs + y * NB + 8 * k) = make_int4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<int4*>(hs + y * NB + 8 * k + 4) = make_int4(o[4], o[5], o[6], o[7]);
         }
-        __syncthreads();  // horizontal squares consumed: the plane area is free
-        if (threadIdx.x == 0) TC_TR(5, clock64());
+        // pre-shifted plane X[y][q][m] = plane[y][8q + m .. 8q + m + 7]; one 16-byte chunk per
+        // item, consecutive lanes on consecutive chunks (conflict-free stores)
         uint8_t* const xop = sm + g.off_x;
         for (int u = threadIdx.x; u < g.PR * NB; u += THREADS) {
             const int y = u >> 6, n = u & 63;
-            *reinterpret_cast<uint4*>(xop + y * XP + (n >> 3) * 128 + (n & 7) * 16) =
-                load16h(pl + y * PCH, n);
+            *reinterpret_cast<uint4*>(xop + y * XP + n * 16) = load16h(pl + y * PCH, n);
         }
+        // A operand (K-major core matrices): reference m's patch row i
         uint8_t* const a_op = sm + g.off_a;
         for (int u = threadIdx.x; u < 128 * P; u += THREADS) {
-            const int m = u >> 3, i = u & 7;
+            const int i = u >> 7, m = u & 127;
             const int row = r + S * (m >> 3) + i, col = r + S * (m & 7);
             *reinterpret_cast<uint4*>(a_op + kmaj16_off(m, i)) = load16h(pl + row * PCH, col);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) TC_TR(5, clock64());
+        // candidate norms N_q = vertical P-sums of hs (<= 64 M^2 < 2^24: exact in fp32)
+        for (int task = threadIdx.x; task < g.NT * 8; task += THREADS) {
+            const int t = task >> 3, k = task & 7;
+            int o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int4 a0 = *reinterpret_cast<const int4*>(hs + (t + i) * NB + 8 * k);
+                const int4 a1 = *reinterpret_cast<const int4*>(hs + (t + i) * NB + 8 * k + 4);
+                o[0] += a0.x; o[1] += a0.y; o[2] += a0.z; o[3] += a0.w;
+                o[4] += a1.x; o[5] += a1.y; o[6] += a1.z; o[7] += a1.w;
+            }
+            *reinterpret_cast<float4*>(nc + t * NB + 8 * k) =
+                make_float4((float)o[0], (float)o[1], (float)o[2], (float)o[3]);
+            *reinterpret_cast<float4*>(nc + t * NB + 8 * k + 4) =
+                make_float4((float)o[4], (float)o[5], (float)o[6], (float)o[7]);
         }
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
@@ -393,9 +499,13 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 ++used;
             }
         } else {
-            uint32_t L[KL];
+            // sorted list of the KP = KL + 1 smallest keys (a power of two for the bulk merge;
+            // the extra slot is never output, the gate is the (K-1)-th key L[KL - 1])
+            constexpr int KP = KL + 1;
+            static_assert((KP & (KP - 1)) == 0 && KP <= 32, "list length must be a power of two");
+            uint32_t L[KP];
 #pragma unroll
-            for (int i = 0; i < KL; ++i) L[i] = KEY_INF;
+            for (int i = 0; i < KP; ++i) L[i] = KEY_INF;
             int nrel = 0;
             if (warp_active) {
                 const int lo = max(wt0, t_lo), hi = min(wt1, t_hi);
@@ -412,7 +522,30 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 uint32_t mlo = hdr.x, mhi = hdr.y;
                 const float GB = (float)(int)hdr.z + 8388608.0f;  // d + 2^23 = v + gate + 2^23
                 const uint32_t code_row = (uint32_t)((int)hdr.w - S * a) * side - (uint32_t)(S * bb);
-                const int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
+                int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
+                if (R >= BULK_MIN) {
+                    // dense row (lists filling): window columns j0 .. j0 + 31 by sort + merge,
+                    // the rest (if any) by the insertion rounds below
+                    const int j0 = S * bb;
+                    const uint64_t mw = ((((uint64_t)mhi) << 32) | mlo) >> j0;
+#pragma unroll
+                    for (int c = 0; c < 32 / KP; ++c) {
+                        uint32_t B[KP];
+#pragma unroll
+                        for (int jj = 0; jj < KP; ++jj) {
+                            const int col = c * KP + jj;
+                            const uint32_t bits =
+                                __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
+                            B[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
+                                                         : KEY_INF;
+                        }
+                        bulk_merge<KP>(L, B);
+                    }
+                    const uint64_t rest = ((((uint64_t)mhi) << 32) | mlo) & ~(0xffffffffull << j0);
+                    mlo = (uint32_t)rest;
+                    mhi = (uint32_t)(rest >> 32);
+                    R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
+                }
                 // next pending candidate (highest column first), software-pipelined one round
                 // ahead of the insertion network
                 auto next_key = [&]() -> uint32_t {
@@ -429,7 +562,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 for (int q = 0; q < R; ++q) {
                     const uint32_t cur = key;
                     key = next_key();
-                    list_insert<KL>(L, cur);
+                    list_insert<KP>(L, cur);
                 }
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sempty[w * NSLOT + slot]);
@@ -457,7 +590,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                     for (int i = 0; i < KL; ++i) {
                         const uint32_t x = other[i];
                         if (!__any_sync(0xffffffffu, x < L[KL - 1])) break;
-                        list_insert<KL>(L, x);
+                        list_insert<KP>(L, x);
                     }
                 }
                 __syncwarp();
