@@ -120,6 +120,26 @@ static __device__ __forceinline__ void bulk_merge(uint32_t (&L)[N], uint32_t (&B
     }
 }
 
+// L (ascending, N keys) <- the N smallest of L and 8 more keys B (any order).
+template <int N>
+static __device__ __forceinline__ void bulk_merge8(uint32_t (&L)[N], uint32_t (&B)[8]) {
+    bitonic_sort<8>(B);
+#pragma unroll
+    for (int i = N - 8; i < N; ++i) L[i] = min(L[i], B[N - 1 - i]);
+#pragma unroll
+    for (int j = N >> 1; j > 0; j >>= 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const int l = i ^ j;
+            if (l > i) {
+                const uint32_t lo = min(L[i], L[l]), hi = max(L[i], L[l]);
+                L[i] = lo;
+                L[l] = hi;
+            }
+        }
+    }
+}
+
 // 8 consecutive fp16 (16 bytes) starting at element c of a 4-byte aligned shared row.
 static __device__ __forceinline__ uint4 load16h(const __half* row, int c) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (c >> 1);
@@ -516,7 +536,9 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             const uint32_t kmul = 1u << cb;
             for (used = hsel; used < nrel; used += NSEL) {
                 const int slot = used % NSLOT;
+                if (lane == 0) TC_TR(5000 + w * 200 + used, clock64());
                 tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
+                if (lane == 0) TC_TR(6000 + w * 200 + used, clock64());
                 const uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                 const uint4 hdr = *reinterpret_cast<const uint4*>(stg + 64);
                 uint32_t mlo = hdr.x, mhi = hdr.y;
@@ -541,7 +563,20 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                         }
                         bulk_merge<KP>(L, B);
                     }
-                    const uint64_t rest = ((((uint64_t)mhi) << 32) | mlo) & ~(0xffffffffull << j0);
+                    uint64_t rest = ((((uint64_t)mhi) << 32) | mlo) & ~(0xffffffffull << j0);
+                    if (2 * r + 1 <= 40) {  // the (at most 8) window columns left: one more batch
+                        uint32_t B8[8];
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const int col = 32 + jj;
+                            const uint32_t bits =
+                                __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
+                            B8[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
+                                                          : KEY_INF;
+                        }
+                        bulk_merge8<KP>(L, B8);
+                        rest = 0ull;
+                    }
                     mlo = (uint32_t)rest;
                     mhi = (uint32_t)(rest >> 32);
                     R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
@@ -558,6 +593,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                     const uint32_t bits = __float_as_uint(__uint_as_float(stg[j]) + GB);
                     return jb >= 0 ? bits * kmul + code_row + (uint32_t)j : KEY_INF;
                 };
+                if (lane == 0) TC_TR(7000 + w * 200 + used, clock64());
                 uint32_t key = next_key();
                 for (int q = 0; q < R; ++q) {
                     const uint32_t cur = key;

@@ -32,3 +32,8 @@ for w in range(4):
     print(f"w{w} staged:", st.tolist())
     print(f"w{w} selector batches (end time):", sel.tolist())
     print(f"w{w} selector R:", rr.tolist())
+
+print("selector phases per row (w0): wait-start, ready, R-known, end")
+for u in range(48):
+    a, b, c_, e = t[5000 + u] - t0, t[6000 + u] - t0, t[7000 + u] - t0, t[3000 + u] - t0
+    print(u, a, b - a, c_ - b, e - c_, "R", t[4000 + u])
