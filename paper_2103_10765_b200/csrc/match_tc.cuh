@@ -181,21 +181,18 @@ static __device__ __noinline__ int tc_exact_ref(const int16_t* __restrict__ img,
 // kernel launched with only_marked = 1 recomputes exactly those tiles.
 constexpr int32_t TC_TILE_MARK = -2;
 
+// One reference tile (bx, by) of image bz; called by the whole CTA.
 template <int S, int KL>
-__global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p, int only_marked) {
+static __device__ __forceinline__ void tc_tile(const MatchParams& p, int bx, int by, int bz) {
     using namespace tcm;
     extern __shared__ __align__(1024) unsigned char sm[];
     const TcGeom g = TcGeom::make(S, p.r);
     constexpr int P = 8;
     const int r = p.r;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int bimg = blockIdx.z;
+    const int bimg = bz;
     const int kr1 = min(p.row_end, p.Ry_reg);
-    const int ky0 = p.row_begin + (int)blockIdx.y * TY, kx0 = (int)blockIdx.x * TX;
-    if (only_marked) {
-        const int64_t ref = (int64_t)bimg * p.out_bstride + (int64_t)(ky0 - p.row_begin) * p.Rx + kx0;
-        if (p.dist[ref * p.K] != TC_TILE_MARK) return;
-    }
+    const int ky0 = p.row_begin + by * TY, kx0 = bx * TX;
     const int gy0 = S * ky0 - r, gx0 = S * kx0 - r;  // global pixel of tile (0, 0)
     const int16_t* __restrict__ img = p.img + (int64_t)bimg * p.img_bstride;
 
@@ -598,6 +595,31 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
 }
 
 // Host launcher over the regular grid part of the call.
+// only_marked = 0: one CTA per tile.  only_marked = 1: a small persistent grid walks all tiles
+// and recomputes the ones the fp16 kernel marked (usually none: a few microseconds).
+template <int S, int KL>
+__global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p, int only_marked) {
+    if (!only_marked) {
+        tc_tile<S, KL>(p, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z);
+        return;
+    }
+    __shared__ int marked;
+    const int kr1 = min(p.row_end, p.Ry_reg);
+    const int nx = (p.Rx_reg + tcm::TX - 1) / tcm::TX, ny = (kr1 - p.row_begin + tcm::TY - 1) / tcm::TY;
+    const int total = nx * ny * p.B;
+    for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
+        const int bx = t % nx, by = (t / nx) % ny, bz = t / (nx * ny);
+        if (threadIdx.x == 0) {
+            const int64_t ref = (int64_t)bz * p.out_bstride + (int64_t)(by * tcm::TY) * p.Rx + bx * tcm::TX;
+            marked = p.dist[ref * p.K] == TC_TILE_MARK;
+        }
+        __syncthreads();
+        const bool m = marked != 0;
+        __syncthreads();
+        if (m) tc_tile<S, KL>(p, bx, by, bz);
+    }
+}
+
 template <int S, int KL>
 cudaError_t launch_tc(const MatchParams& p, cudaStream_t stream, int* launches, int only_marked) {
     const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
@@ -607,6 +629,17 @@ cudaError_t launch_tc(const MatchParams& p, cudaStream_t stream, int* launches, 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.total);
     if (e != cudaSuccess) return e;
     dim3 grid((p.Rx_reg + tcm::TX - 1) / tcm::TX, (kr1 - kr0 + tcm::TY - 1) / tcm::TY, p.B);
+    if (only_marked) {
+        static int n_sm = 0;
+        if (n_sm == 0) {
+            int dev = 0;
+            if (cudaGetDevice(&dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+                n_sm = 148;
+        }
+        const long long tiles = (long long)grid.x * grid.y * grid.z;
+        grid = dim3((unsigned)(tiles < n_sm ? tiles : n_sm), 1, 1);
+    }
     kern<<<grid, tcm::THREADS, g.total, stream>>>(p, only_marked);
     if (launches) ++*launches;
     return cudaGetLastError();
