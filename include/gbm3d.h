@@ -106,8 +106,11 @@ int gbm3d_block_match_ex(const int16_t* imgs, int B, int H, int W, int patch, in
 
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
- * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out
- * on `stream`, and BLOCKS until the results are on the host. */
+ * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,
+ * and BLOCKS until the results are on the host.  The work is pipelined in up to 8 chunks
+ * (images for B > 1, blocks of reference rows for B = 1): copies run on two library-owned
+ * streams (created once per host thread) overlapped with the matching on `stream`.
+ * Results are identical to the device entries. */
 size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, int K);
 int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,
                            int radius, int K, int64_t tau, int32_t* h_idx, int32_t* h_dist,

@@ -250,6 +250,37 @@ size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, in
     return img + 2 * tab + nv;
 }
 
+// Host entry, pipelined: the job is cut into chunks (images for B > 1, blocks of reference
+// rows for B = 1); the host-to-device copies run on one library stream, the matching of chunk
+// c alternately on the caller's stream and a second compute stream (consecutive chunks may
+// overlap on the SMs, so no chunk ends on a partial wave), and the device-to-host copies of
+// chunk c on a third stream while later chunks are matched.  PCIe is full duplex, so
+// the copies hide behind each other and behind the kernels.  The library streams and events
+// are created once per host thread (thread_local) and reused; nothing else is allocated.
+namespace {
+constexpr int kMaxChunks = 16;
+struct HostPipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp2 = nullptr;
+    cudaEvent_t in[kMaxChunks], done[kMaxChunks], out_done, start;
+    bool ok = false;
+    bool init() {
+        if (ok) return true;
+        if (cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaStreamCreateWithFlags(&comp2, cudaStreamNonBlocking) != cudaSuccess) return false;
+        for (int i = 0; i < kMaxChunks; ++i) {
+            if (cudaEventCreateWithFlags(&in[i], cudaEventDisableTiming) != cudaSuccess) return false;
+            if (cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) != cudaSuccess) return false;
+        }
+        if (cudaEventCreateWithFlags(&out_done, cudaEventDisableTiming) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess) return false;
+        ok = true;
+        return true;
+    }
+};
+thread_local HostPipe g_pipe;
+}  // namespace
+
 int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,
                            int radius, int K, int64_t tau, int32_t* h_idx, int32_t* h_dist,
                            int32_t* h_n_valid, void* d_workspace, size_t workspace_bytes,
@@ -260,29 +291,78 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
     MatchParams p;
     int st = make_params(p, B, H, W, patch, stride, radius, K, tau);
     if (st != GBM3D_OK) return st;
+    if (!g_pipe.init()) return GBM3D_ERR_CUDA;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
     const size_t img_b = (size_t)B * H * W * 2;
-    const size_t nref = (size_t)B * p.Ry * p.Rx;
+    const size_t per_img_refs = (size_t)p.Ry * p.Rx;
+    const size_t nref = (size_t)B * per_img_refs;
     int16_t* d_img = (int16_t*)ws;
     int32_t* d_idx = (int32_t*)(ws + ((img_b + 255) & ~(size_t)255));
     int32_t* d_dist = (int32_t*)((char*)d_idx + ((nref * K * 4 + 255) & ~(size_t)255));
     int32_t* d_nv = (int32_t*)((char*)d_dist + ((nref * K * 4 + 255) & ~(size_t)255));
-    if (cudaMemcpyAsync(d_img, h_imgs, img_b, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    // chunk plan: [u0, u1) in images (B > 1) or in reference rows (B = 1, multiples of 16 so
+    // the tensor-core tiles of a chunk are the tiles of the whole call)
+    const int units = B > 1 ? B : p.Ry;
+    int nch = B > 1 ? std::min(B, 8) : std::min(8, std::max(1, p.Ry / 64));
+    int step = (units + nch - 1) / nch;
+    if (B == 1) step = (step + 15) & ~15;
+    nch = (units + step - 1) / step;
+    if (nch > kMaxChunks) return GBM3D_ERR_ARG;  // unreachable: at most 8 chunks
+    int launches = 0;
+    // the library streams start after whatever the caller queued before this call
+    if (cudaEventRecord(g_pipe.start, s) != cudaSuccess ||
+        cudaStreamWaitEvent(g_pipe.h2d, g_pipe.start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(g_pipe.comp2, g_pipe.start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(g_pipe.d2h, g_pipe.start, 0) != cudaSuccess)
         return GBM3D_ERR_CUDA;
-    p.img = d_img;
-    p.idx = d_idx;
-    p.dist = d_dist;
-    p.nvalid = d_nv;
-    st = run(p, GBM3D_METHOD_AUTO, s);
-    if (st != GBM3D_OK) return st;
-    if (cudaMemcpyAsync(h_idx, d_idx, nref * K * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return GBM3D_ERR_CUDA;
-    if (cudaMemcpyAsync(h_dist, d_dist, nref * K * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return GBM3D_ERR_CUDA;
-    if (h_n_valid &&
-        cudaMemcpyAsync(h_n_valid, d_nv, nref * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return GBM3D_ERR_CUDA;
+    // pixels in: per image chunk (B > 1) or the whole image (B = 1)
+    for (int c = 0; c < (B > 1 ? nch : 1); ++c) {
+        const int b0 = B > 1 ? c * step : 0, b1 = B > 1 ? std::min(B, b0 + step) : 1;
+        const size_t off = (size_t)b0 * H * W, n = (size_t)(b1 - b0) * H * W * 2;
+        if (cudaMemcpyAsync(d_img + off, h_imgs + off, n, cudaMemcpyHostToDevice, g_pipe.h2d) != cudaSuccess)
+            return GBM3D_ERR_CUDA;
+        if (cudaEventRecord(g_pipe.in[c], g_pipe.h2d) != cudaSuccess) return GBM3D_ERR_CUDA;
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int u0 = c * step, u1 = std::min(units, u0 + step);
+        cudaStream_t cs = (c & 1) ? g_pipe.comp2 : s;
+        if (cudaStreamWaitEvent(cs, g_pipe.in[B > 1 ? c : 0], 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+        MatchParams q = p;
+        size_t r0, nr;  // first reference and reference count of the chunk in the outputs
+        if (B > 1) {
+            q.B = u1 - u0;
+            q.img = d_img + (size_t)u0 * H * W;
+            r0 = (size_t)u0 * per_img_refs;
+            nr = (size_t)(u1 - u0) * per_img_refs;
+        } else {
+            q.img = d_img;
+            q.row_begin = u0;
+            q.row_end = u1;
+            q.out_bstride = (int64_t)(u1 - u0) * p.Rx;
+            r0 = (size_t)u0 * p.Rx;
+            nr = (size_t)(u1 - u0) * p.Rx;
+        }
+        q.idx = d_idx + r0 * K;
+        q.dist = d_dist + r0 * K;
+        q.nvalid = d_nv + r0;
+        st = run(q, GBM3D_METHOD_AUTO, cs);
+        if (st != GBM3D_OK) return st;
+        launches += g_last_launches;
+        if (cudaEventRecord(g_pipe.done[c], cs) != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (cudaStreamWaitEvent(g_pipe.d2h, g_pipe.done[c], 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (cudaMemcpyAsync(h_idx + r0 * K, q.idx, nr * K * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess ||
+            cudaMemcpyAsync(h_dist + r0 * K, q.dist, nr * K * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
+            return GBM3D_ERR_CUDA;
+        if (h_n_valid &&
+            cudaMemcpyAsync(h_n_valid + r0, q.nvalid, nr * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
+            return GBM3D_ERR_CUDA;
+    }
+    g_last_launches = launches;
+    // the caller's stream is ordered after the copies out (which follow every chunk's
+    // matching), then the call blocks on it
+    if (cudaEventRecord(g_pipe.out_done, g_pipe.d2h) != cudaSuccess) return GBM3D_ERR_CUDA;
+    if (cudaStreamWaitEvent(s, g_pipe.out_done, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess) return GBM3D_ERR_CUDA;
     return GBM3D_OK;
 }
