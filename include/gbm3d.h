@@ -15,10 +15,17 @@
  *   local window, "exactly 15 matches" for K = 16 (R4).  Missing slots are
  *   "padded with the reference block": idx = idx(rho), dist = -1 (R7).
  *   idx(c) = cy * W + cx (raster index of the candidate's top-left pixel).
- *   The kernels evaluate d organised by displacement delta = c - rho: the shifted-difference
- *   image (Z - S_delta Z)^2 box-summed over P x P (Prop. 1 with an all-ones block,
- *   PAPER.md:89-113), in exact int32 arithmetic -- results are bit-identical to the
- *   definition above.
+ *   Two exact formulations compute d (results are bit-identical to the definition above):
+ *   - product form (Eq. (2): d = ||f_p||^2 + ||f_q||^2 - 2 <f_p, f_q>), the AUTO
+ *     choice for patch 8 / stride 3 / radius <= 21 / K <= 32: the inner products of a tile of
+ *     128 references with each candidate row run on the tcgen05 tensor cores (fp16 operands of
+ *     tile-centred pixels, fp32 accumulators; every partial sum is an integer below 2^24, so
+ *     exact; tiles whose pixel range breaks that bound are redone by an int8 byte-plane
+ *     kernel), norms by box sums (step 1);
+ *   - SSD form, organised by displacement delta = c - rho: the shifted-difference image
+ *     (Z - S_delta Z)^2 box-summed over P x P (Prop. 1 with an all-ones block,
+ *     PAPER.md:89-113), in int32; used for the other instantiated shapes.
+ *   Anything else runs the direct per-reference kernel.
  *
  * Layouts (all row-major, contiguous):
  *   image      int16  [H][W]          batched: [B][H][W]
@@ -64,7 +71,7 @@ enum {
 enum {
     GBM3D_METHOD_AUTO = 0,     /* fastest exact kernel available for the shape            */
     GBM3D_METHOD_SSD = 1,      /* displacement-organised shifted-difference box sums      */
-    GBM3D_METHOD_PRODUCT = 2,  /* Eq. (2) product form: norms + box sums of Z * S_delta Z */
+    GBM3D_METHOD_PRODUCT = 2,  /* Eq. (2) product form on tensor cores (fp16, exact)      */
     GBM3D_METHOD_DIRECT = 3,   /* generic per-reference direct SSD (any shape; slow)      */
     GBM3D_METHOD_PRODUCT_I8 = 4 /* product form, byte-plane int8 tensor-core kernel only   */
 };
