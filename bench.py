@@ -290,6 +290,7 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
         "clocks": clocks,
         "kernel_ms": {"mean": ms, "min": min(times), "max": max(times)},
     }
+    line["gather"] = run_gather(args, cfg, call, torch, g, img, outs[0], flush_buf)
     if want_e2e:
         line["e2e"] = run_e2e(args, cfg, call, torch, g)
     if want_cpu:
@@ -300,6 +301,28 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
                                 "gevals_per_s": evr / 1e9}
     del imgs, outs, flush_buf
     return line
+
+
+def run_gather(args, cfg, call, torch, g, img, idx, flush_buf):
+    """the matched-block groups (5D tensor of PAPER.md:217) from this step's table,
+    timed like the step (events, L2 flushed between launches).  HBM-write bound: roofline
+    bytes = groups written + table read + image read, against MEASURED_PEAKS hbm_gbs."""
+    grp = torch.empty(tuple(idx.shape) + (call.patch, call.patch), dtype=torch.int16,
+                      device=idx.device)
+
+    def step():
+        g.gather_groups(img, idx, call.patch, out=grp)
+
+    times = measure_device(step, args.steps, args.warmup, flush_buf.zero_, torch, soak_s=0.2)
+    ms = statistics.mean(times)
+    nbytes = grp.numel() * 2 + idx.numel() * 4 + img.numel() * 2
+    peak, src = measured_peak("hbm_gbs", 7672.0)
+    ach = nbytes / (ms * 1e-3) / 1e9
+    del grp
+    return {"what": "gbm3d_gather_groups: [.., K, P, P] int16 blocks of the step's table",
+            "ms": ms, "blocks_per_s": idx.numel() / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "bytes_per_launch": nbytes, "peak_source": src}}
 
 
 def run_e2e(args, cfg, call, torch, g):
@@ -372,7 +395,7 @@ def main():
         line["also"] = {"c4": {k: also[k] for k in ("value", "unit", "ms_per_step",
                                                     "gevals_per_s", "roofline",
                                                     "roofline_tensor", "e2e", "config",
-                                                    "clocks", "gpu_launches")}}
+                                                    "clocks", "gpu_launches", "gather")}}
     print(json.dumps(line), flush=True)
 
 

@@ -111,6 +111,31 @@ int gbm3d_block_match_ex(const int16_t* imgs, int B, int H, int W, int patch, in
                          int radius, int K, int64_t tau, int method, int32_t* idx,
                          int32_t* dist, int32_t* n_valid, void* stream);
 
+/* ---- Matched-block gather (the groups the 3D filtering of both stages
+ * consumes).  imgs: device int16 [B][H][W] (4-byte aligned, as cudaMalloc returns); idx:
+ * device int32 tables of gbm3d_block_match* for the same (B, H, W, patch).
+ *
+ * gbm3d_gather_groups: the 5D tensor of PAPER.md:217 ("N x N x K x B x B": matched blocks x
+ * reference grid), layout groups[b][ry][rx][k][i][j] = Z_b[cy + i][cx + j] with
+ * (cy, cx) = (idx[b][ry][rx][k] / W, idx[b][ry][rx][k] % W), 0 <= i, j < patch, for the
+ * table shape [B][Ry][Rx][K].  Pad slots hold the reference's own index, so they repeat the
+ * reference block ("padded with the reference block").  Fast path (patch 8):
+ * each CTA stages the bounding box of a 64-reference strip's candidates in shared memory.
+ *
+ * gbm3d_gather_volume: the paper's volume of matched blocks for tiling references
+ * (stride = patch = N, N | H and N | W):
+ *   vol[b][k][p N + i][q N + j] = Z_b[cy + i][cx + j],  (cy, cx) from idx[b][p Bx + q][k],
+ * i.e. V[pN+i, qN+j, z] of PAPER.md:162 stored slice-major ([B][K][H][W]); slice 0 is Z.
+ *
+ * Both enqueue on `stream`, allocate nothing, and are bit-exact copies (an index outside the
+ * image writes a zero block).  Errors: GBM3D_ERR_ARG for null pointers / bad sizes (and, for
+ * the volume, H or W not a multiple of patch); GBM3D_ERR_UNSUPPORTED for patch > 16;
+ * GBM3D_ERR_CUDA for a launch error. */
+int gbm3d_gather_groups(const int16_t* imgs, int B, int H, int W, int patch, const int32_t* idx,
+                        int Ry, int Rx, int K, int16_t* groups, void* stream);
+int gbm3d_gather_volume(const int16_t* imgs, int B, int H, int W, int patch, const int32_t* idx,
+                        int K, int16_t* vol, void* stream);
+
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
  * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,

@@ -142,3 +142,46 @@ def block_match_batched(imgs: np.ndarray, patch: int, stride: int, radius: int, 
                         tau: Optional[int] = None, threads: int = 0):
     outs = [block_match(im, patch, stride, radius, K, tau, threads) for im in imgs]
     return tuple(np.stack([o[i] for o in outs]) for i in range(3))
+
+
+def gather_groups(img: np.ndarray, idx: np.ndarray, patch: int) -> np.ndarray:
+    """The matched blocks of every reference, stacked as the paper's 5D tensor "N x N x K x B x B"
+    (the blocks of S^K_pq): out[.., r, k] = Z[cy:cy+N, cx:cx+N] with
+    (cy, cx) = divmod(idx[.., r, k], W).  Written as the plain slice copy it is."""
+    img = np.asarray(img)
+    idx = np.asarray(idx)
+    batched = img.ndim == 3
+    imgs = img if batched else img[None]
+    tabs = idx if batched else idx[None]
+    B, H, W = imgs.shape
+    out = np.zeros(tabs.shape + (patch, patch), dtype=np.int16)
+    for b in range(B):
+        flat = tabs[b].reshape(-1)
+        o = out[b].reshape(-1, patch, patch)
+        for n, c in enumerate(flat):
+            cy, cx = divmod(int(c), W)
+            o[n] = imgs[b, cy:cy + patch, cx:cx + patch]
+    return out if batched else out[0]
+
+
+def gather_volume(img: np.ndarray, idx: np.ndarray, patch: int) -> np.ndarray:
+    """The aggregated 3D volume of matched blocks, for tiling references
+    (stride = N, N | M): V[p N + i, q N + j, z] = Z_x[i, j] with x the z-th match of tile (p, q).
+    Returned slice-major: out[.., z, y, x] = V[y, x, z]."""
+    img = np.asarray(img)
+    idx = np.asarray(idx)
+    batched = img.ndim == 3
+    imgs = img if batched else img[None]
+    tabs = idx if batched else idx[None]
+    B, H, W = imgs.shape
+    N = patch
+    K = tabs.shape[-1]
+    V = np.zeros((B, H, W, K), dtype=np.int16)  # the paper's index order [x, y, z]
+    for b in range(B):
+        for p in range(H // N):
+            for q in range(W // N):
+                for z in range(K):
+                    cy, cx = divmod(int(tabs[b, p, q, z]), W)
+                    V[b, p * N:(p + 1) * N, q * N:(q + 1) * N, z] = imgs[b, cy:cy + N, cx:cx + N]
+    out = np.ascontiguousarray(np.moveaxis(V, 3, 1))
+    return out if batched else out[0]

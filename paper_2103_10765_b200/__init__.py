@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 __all__ = [
     "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
     "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
-    "last_launch_count", "version",
+    "last_launch_count", "version", "gather_groups", "gather_volume",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -60,6 +60,8 @@ def load_library():
         "gbm3d_block_match_host": (i32, [vp, i32, i32, i32, i32, i32, i32, i32, i64, vp, vp, vp,
                                          vp, ctypes.c_size_t, vp]),
         "gbm3d_check_range": (i32, [vp, i64, i32, ip, vp]),
+        "gbm3d_gather_groups": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp]),
+        "gbm3d_gather_volume": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, vp]),
         "gbm3d_last_launch_count": (i32, []),
         "gbm3d_strerror": (ctypes.c_char_p, [i32]),
         "gbm3d_version": (ctypes.c_char_p, []),
@@ -220,4 +222,64 @@ def block_match_host(h_img, patch: int, stride: int, radius: int, K: int,
         _stream_handle(device))
     if st != 0:
         raise GBM3DError(st, "block_match_host")
+    return out
+
+
+def _check_cuda_int32(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int32:
+        raise TypeError(f"{name} must be a CUDA torch.int32 tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def gather_groups(img, idx, patch: int, out=None):
+    """Matched-block groups (the 5D tensor of PAPER.md:217): for a table ``idx`` [(B,) Ry, Rx, K]
+    of ``block_match`` on ``img`` [(B,) H, W], returns int16 [(B,) Ry, Rx, K, patch, patch] with
+    block k of reference (y, x) = the patch whose top-left raster index is idx[.., y, x, k]."""
+    import torch
+    _check_cuda_int16(img, "img")
+    _check_cuda_int32(idx, "idx")
+    batched = img.dim() == 3
+    B = img.shape[0] if batched else 1
+    H, W = img.shape[-2], img.shape[-1]
+    if idx.dim() != (4 if batched else 3) or (batched and idx.shape[0] != B):
+        raise ValueError("idx must be [(B,) Ry, Rx, K] matching img")
+    Ry, Rx, K = idx.shape[-3], idx.shape[-2], idx.shape[-1]
+    shape = tuple(idx.shape) + (patch, patch)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int16, device=img.device)
+    elif out.dtype != torch.int16 or tuple(out.shape) != shape or not out.is_contiguous():
+        raise ValueError(f"out must be contiguous int16 {shape}")
+    st = load_library().gbm3d_gather_groups(
+        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), Ry,
+        Rx, K, ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
+    if st != 0:
+        raise GBM3DError(st, "gather_groups")
+    return out
+
+
+def gather_volume(img, idx, patch: int, out=None):
+    """The volume of matched blocks V for tiling references (stride = patch,
+    patch | H, W): returns int16 [(B,) K, H, W] with slice k = the k-th matched block of every
+    tile placed at the tile's position (slice 0 is the image itself)."""
+    import torch
+    _check_cuda_int16(img, "img")
+    _check_cuda_int32(idx, "idx")
+    batched = img.dim() == 3
+    B = img.shape[0] if batched else 1
+    H, W = img.shape[-2], img.shape[-1]
+    K = idx.shape[-1]
+    if idx.shape[-3:-1] != (H // patch, W // patch):
+        raise ValueError("idx must be the table of the tiling grid (stride = patch)")
+    shape = ((B,) if batched else ()) + (K, H, W)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int16, device=img.device)
+    elif out.dtype != torch.int16 or tuple(out.shape) != shape or not out.is_contiguous():
+        raise ValueError(f"out must be contiguous int16 {shape}")
+    st = load_library().gbm3d_gather_volume(
+        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), K,
+        ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
+    if st != 0:
+        raise GBM3DError(st, "gather_volume")
     return out

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "../../include/gbm3d.h"
@@ -122,6 +123,13 @@ static cudaError_t launch_direct(const MatchParams& p, cudaStream_t st, int k_be
 
 // Dispatch one call: strip kernel over the regular grid part, direct kernel for the appended
 // row/column (reading R3), or direct for everything when no fast kernel fits.
+// GBM3D_DEBUG=1 prints the CUDA error behind a GBM3D_ERR_CUDA status (stderr).
+static int cuda_fail(cudaError_t e, const char* where) {
+    static const bool dbg = getenv("GBM3D_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "gbm3d: %s: %s\n", where, cudaGetErrorString(e));
+    return GBM3D_ERR_CUDA;
+}
+
 static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
@@ -130,12 +138,12 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
         method == GBM3D_METHOD_PRODUCT_I8) {
         // AUTO prefers the tensor-core product form (fastest where it applies)
         e = tc_dispatch(p, st, &launches, &fast, method == GBM3D_METHOD_PRODUCT_I8);
-        if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (e != cudaSuccess) return cuda_fail(e, "tensor-core kernels");
         if (!fast && method != GBM3D_METHOD_AUTO) return GBM3D_ERR_UNSUPPORTED;
     }
     if (!fast && (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_SSD)) {
         e = strip_dispatch(p, st, &launches, &fast);
-        if (e != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (e != cudaSuccess) return cuda_fail(e, "strip kernel");
         if (!fast && method == GBM3D_METHOD_SSD) return GBM3D_ERR_UNSUPPORTED;
     }
     if (fast) {

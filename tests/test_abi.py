@@ -87,3 +87,25 @@ def test_product_path_never_imports_oracle():
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), fn
                 assert "liboracle" not in txt and "gbm3d_oracle" not in txt, fn
+
+
+def test_gather_argument_validation_host():
+    """gather entries reject bad arguments before any CUDA call (runs without a GPU)."""
+    g, lib = _lib()
+    d = ctypes.c_void_p(0x1000)
+    null = ctypes.c_void_p(0)
+    G, V = lib.gbm3d_gather_groups, lib.gbm3d_gather_volume
+    # (imgs, B, H, W, patch, idx, Ry, Rx, K, groups, stream)
+    assert G(null, 1, 64, 64, 8, d, 20, 20, 16, d, null) == -1
+    assert G(d, 1, 64, 64, 8, null, 20, 20, 16, d, null) == -1
+    assert G(d, 0, 64, 64, 8, d, 20, 20, 16, d, null) == -1
+    assert G(d, 1, 7, 64, 8, d, 20, 20, 16, d, null) == -1
+    assert G(d, 1, 64, 64, 8, d, 20, 20, 0, d, null) == -1
+    assert G(d, 1, 64, 64, 8, d, -1, 20, 16, d, null) == -1
+    assert G(d, 1, 64, 64, 17, d, 20, 20, 16, d, null) == -3
+    assert G(d, 1, 64, 64, 8, d, 0, 20, 16, d, null) == 0  # nothing to do
+    # (imgs, B, H, W, patch, idx, K, vol, stream): tiling needs patch | H and patch | W
+    assert V(d, 1, 60, 64, 8, d, 16, d, null) == -1
+    assert V(d, 1, 64, 60, 8, d, 16, d, null) == -1
+    assert V(d, 1, 64, 64, 8, null, 16, d, null) == -1
+    assert V(d, 1, 64, 64, 32, d, 16, d, null) == -3
