@@ -79,6 +79,19 @@ struct Tc16Geom {
     }
 };
 
+// Two keys into a sorted list of N in one pass: the k-th smallest of L and {lo <= hi} is
+// min(L[k], max(L[k-1], lo), max(L[k-2], hi)) (merge of sorted lists), i.e. two max and one
+// 3-input min (VIMNMX3) per element -- 1.5 ALU ops per key and element instead of 2, and the
+// two keys share one dependency chain (tools/dev/insert_bench.cu: 1.5x keys per cycle).
+template <int N>
+static __device__ __forceinline__ void list_insert2(uint32_t (&L)[N], uint32_t x, uint32_t y) {
+    const uint32_t lo = min(x, y), hi = max(x, y);
+#pragma unroll
+    for (int i = N - 1; i >= 2; --i) L[i] = __vimin3_u32(L[i], max(L[i - 1], lo), max(L[i - 2], hi));
+    L[1] = __vimin3_u32(L[1], max(L[0], lo), hi);
+    L[0] = min(L[0], lo);
+}
+
 // Ascending bitonic sort of N (power of two) register keys; fully unrolled min/max network.
 template <int N>
 static __device__ __forceinline__ void bitonic_sort(uint32_t (&B)[N]) {
@@ -594,11 +607,13 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                     return jb >= 0 ? bits * kmul + code_row + (uint32_t)j : KEY_INF;
                 };
                 if (lane == 0) TC_TR(7000 + w * 200 + used, clock64());
-                uint32_t key = next_key();
-                for (int q = 0; q < R; ++q) {
-                    const uint32_t cur = key;
-                    key = next_key();
-                    list_insert<KP>(L, cur);
+                // two pending keys per round (the second is KEY_INF when a lane has run out)
+                uint32_t ka = next_key(), kb = next_key();
+                for (int q = 0; q < (R + 1) >> 1; ++q) {
+                    const uint32_t ca = ka, cb2 = kb;
+                    ka = next_key();
+                    kb = next_key();
+                    list_insert2<KP>(L, ca, cb2);
                 }
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sempty[w * NSLOT + slot]);
