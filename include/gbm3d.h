@@ -136,6 +136,27 @@ int gbm3d_gather_groups(const int16_t* imgs, int B, int H, int W, int patch, con
 int gbm3d_gather_volume(const int16_t* imgs, int B, int H, int W, int patch, const int32_t* idx,
                         int K, int16_t* vol, void* stream);
 
+/* ---- Stage-2 collaborative Wiener filtering + aggregation (PAPER.md:210-217,
+ * aggregation Eq. of PAPER.md:190 with the original algorithm's Wiener weights).
+ * noisy: device int16 [B][H][W]; basic: device float32 [B][H][W] (the basic estimate the
+ * shrinkage is computed from); idx / n_valid: device tables [B][Ry][Rx][K] / [B][Ry][Rx] of
+ * gbm3d_block_match* for the same (B, H, W, patch) -- their indices must lie in the image;
+ * sigmas: device float32 [B] noise standard deviations; out: device float32 [B][H][W].
+ * For every group: T = Haar_K o DCT2_8x8 (orthonormal) of the noisy and of the basic blocks,
+ * W = T_B^2 / (T_B^2 + sigma^2) (1 where both vanish), filtered blocks T^-1(W . T_Z), group
+ * weight 1 / (sigma^2 ||W||^2) (1 if sigma = 0 or ||W|| = 0); out = weighted average of the
+ * filtered blocks over every pixel, using the first n_valid blocks of each group (pad blocks
+ * are left out).  fp32 arithmetic with atomic accumulation: results match a
+ * float64 evaluation within DESIGN.md's tolerance, not bit for bit.
+ * workspace: device buffer of gbm3d_wiener_workspace_bytes(B, H, W) bytes (2 float planes),
+ * cleared by the call.  Errors: GBM3D_ERR_ARG (null pointer, sizes, small workspace),
+ * GBM3D_ERR_UNSUPPORTED (patch != 8, K not a power of two or > 32), GBM3D_ERR_CUDA. */
+size_t gbm3d_wiener_workspace_bytes(int B, int H, int W);
+int gbm3d_wiener_stage2(const int16_t* noisy, const float* basic, int B, int H, int W, int patch,
+                        const int32_t* idx, const int32_t* n_valid, int Ry, int Rx, int K,
+                        const float* sigmas, float* out, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
  * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,

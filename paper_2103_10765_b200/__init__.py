@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 __all__ = [
     "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
     "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
-    "last_launch_count", "version", "gather_groups", "gather_volume",
+    "last_launch_count", "version", "gather_groups", "gather_volume", "wiener_stage2",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -62,6 +62,9 @@ def load_library():
         "gbm3d_check_range": (i32, [vp, i64, i32, ip, vp]),
         "gbm3d_gather_groups": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp]),
         "gbm3d_gather_volume": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, vp]),
+        "gbm3d_wiener_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32]),
+        "gbm3d_wiener_stage2": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp,
+                                      vp, ctypes.c_size_t, vp]),
         "gbm3d_last_launch_count": (i32, []),
         "gbm3d_strerror": (ctypes.c_char_p, [i32]),
         "gbm3d_version": (ctypes.c_char_p, []),
@@ -282,4 +285,38 @@ def gather_volume(img, idx, patch: int, out=None):
         ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "gather_volume")
+    return out
+
+
+def wiener_stage2(noisy, basic, idx, n_valid, patch: int, sigma, out=None, workspace=None):
+    """Stage-2 collaborative Wiener estimate from the match
+    tables of ``block_match`` (normally run on the basic estimate): noisy int16 and basic
+    float32 CUDA tensors [(B,) H, W], sigma a float or one per image.  Returns float32 [(B,) H, W]."""
+    import torch
+    _check_cuda_int16(noisy, "noisy")
+    _check_cuda_int32(idx, "idx")
+    _check_cuda_int32(n_valid, "n_valid")
+    if basic.dtype != torch.float32 or not basic.is_cuda or basic.shape != noisy.shape \
+            or not basic.is_contiguous():
+        raise TypeError("basic must be a contiguous CUDA float32 tensor shaped like noisy")
+    batched = noisy.dim() == 3
+    B = noisy.shape[0] if batched else 1
+    H, W = noisy.shape[-2], noisy.shape[-1]
+    Ry, Rx, K = idx.shape[-3], idx.shape[-2], idx.shape[-1]
+    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
+    if sig.numel() == 1:
+        sig = sig.expand(B)
+    sig = sig.contiguous().to(noisy.device)
+    if out is None:
+        out = torch.empty(noisy.shape, dtype=torch.float32, device=noisy.device)
+    need = int(load_library().gbm3d_wiener_workspace_bytes(B, H, W))
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=noisy.device)
+    st = load_library().gbm3d_wiener_stage2(
+        ctypes.c_void_p(noisy.data_ptr()), ctypes.c_void_p(basic.data_ptr()), B, H, W, patch,
+        ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(n_valid.data_ptr()), Ry, Rx, K,
+        ctypes.c_void_p(sig.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_handle(noisy.device))
+    if st != 0:
+        raise GBM3DError(st, "wiener_stage2")
     return out
