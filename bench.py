@@ -359,7 +359,10 @@ def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
     ms = statistics.mean(times)
     blocks = idx.numel()
     lg = int(math.log2(call.K))
-    flops_blk = 3 * 2 * 2 * 512 + 3 * 64 * lg * 2 + 64 * 6
+    # per block: three 2D DCTs as 16 even/odd 8-point transforms (8 adds + 32 FMA = 72 flops),
+    # three Haar cascades (64 coefficients x log2 K levels x 2 flops, counted for every lane),
+    # shrinkage and product (64 x 6), weighted numerator (64 x 2)
+    flops_blk = 3 * 16 * 72 + 3 * 64 * lg * 2 + 64 * 6 + 64 * 2
     ach = blocks * flops_blk / (ms * 1e-3) / 1e12
     sm_max = 1965.0
     peak = FP32_FMA_LANES_PER_SM * 2 * N_SMS * sm_max * 1e6 / 1e12

@@ -31,37 +31,58 @@ namespace {
 
 constexpr int WT = 8;                   // reference tile: WT x WT grid cells per CTA
 constexpr int WTHREADS = 128;
-constexpr int REGION_MAX = 6144;        // pixels of the shared aggregation region (48 KB)
+constexpr int REGION_MAX = 6144;        // pixels of the shared aggregation region (3 x 24 KB)
 
-__device__ __forceinline__ void dct8_rows(float (&x)[64], const float* __restrict__ C, bool inverse) {
-    // rows: y[i][k] = sum_j C[k][j] x[i][j]   (inverse: sum_j C[j][k] x[i][j])
+// 8-point orthonormal DCT-II of v[0], v[st], .., v[7 st] in place, by the symmetry of its
+// rows: even rows see s_j = x_j + x_{7-j}, odd rows d_j = x_j - x_{7-j} (4 products each
+// instead of 8).  The inverse (DCT-III) splits the same way: x_j = E_j + O_j, x_{7-j} = E_j - O_j.
+__device__ __forceinline__ void dct8_1d(float* v, int st, const float* __restrict__ C, bool inverse) {
+    if (!inverse) {
+        float sj[4], dj[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        float y[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            float s = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s = fmaf(inverse ? C[j * 8 + k] : C[k * 8 + j], x[i * 8 + j], s);
-            y[k] = s;
+        for (int j = 0; j < 4; ++j) {
+            sj[j] = v[j * st] + v[(7 - j) * st];
+            dj[j] = v[j * st] - v[(7 - j) * st];
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[i * 8 + k] = y[k];
+        for (int k = 0; k < 8; ++k) {
+            const float* src = (k & 1) ? dj : sj;
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc = fmaf(C[k * 8 + j], src[j], acc);
+            v[k * st] = acc;
+        }
+    } else {
+        float e[4], o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float ae = 0.f, ao = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) ae = fmaf(C[k * 8 + j], v[k * st], ae);
+#pragma unroll
+            for (int k = 1; k < 8; k += 2) ao = fmaf(C[k * 8 + j], v[k * st], ao);
+            e[j] = ae;
+            o[j] = ao;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j * st] = e[j] + o[j];
+            v[(7 - j) * st] = e[j] - o[j];
+        }
     }
 }
-__device__ __forceinline__ void dct8_cols(float (&x)[64], const float* __restrict__ C, bool inverse) {
+// 2D: rows then columns (forward), columns then rows (inverse) of the 8 x 8 block x[i * 8 + j].
+__device__ __forceinline__ void dct8x8(float (&x)[64], const float* __restrict__ C, bool inverse) {
+    if (!inverse) {
 #pragma unroll
-    for (int l = 0; l < 8; ++l) {
-        float y[8];
+        for (int i = 0; i < 8; ++i) dct8_1d(x + 8 * i, 1, C, false);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            float s = 0.f;
+        for (int l = 0; l < 8; ++l) dct8_1d(x + l, 8, C, false);
+    } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s = fmaf(inverse ? C[i * 8 + k] : C[k * 8 + i], x[i * 8 + l], s);
-            y[k] = s;
-        }
+        for (int l = 0; l < 8; ++l) dct8_1d(x + l, 8, C, true);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k * 8 + l] = y[k];
+        for (int i = 0; i < 8; ++i) dct8_1d(x + 8 * i, 1, C, true);
     }
 }
 
@@ -93,8 +114,9 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid, int Ry, int Rx,
         const float* __restrict__ sigmas, float* __restrict__ num, float* __restrict__ den) {
     extern __shared__ float wsm[];
-    float* const rnum = wsm;                   // [REGION_MAX]
-    float* const rden = wsm + REGION_MAX;      // [REGION_MAX]
+    float* const rnum = wsm;                   // [REGION_MAX] numerator sums
+    float* const rwm = wsm + REGION_MAX;       // [REGION_MAX] block weights at block top-lefts
+    float* const rtmp = wsm + 2 * REGION_MAX;  // [REGION_MAX] horizontal box sums of rwm
     __shared__ float C[64];
     __shared__ int bb[4];
     const int b = blockIdx.z;
@@ -128,7 +150,7 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
     const int rh = bb[1] + 8 - by0, rw = bb[3] + 8 - bx0;
     const bool regional = rh * rw <= REGION_MAX;
     if (regional)
-        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) { rnum[i] = 0.f; rden[i] = 0.f; }
+        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) { rnum[i] = 0.f; rwm[i] = 0.f; }
     __syncthreads();
 
     constexpr int GPW = 32 / K;  // groups per warp pass
@@ -149,8 +171,7 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) tb[i * 8 + j] = __ldg(bimg + (int64_t)(cy + i) * W + cx + j);
-        dct8_rows(tb, C, false);
-        dct8_cols(tb, C, false);
+        dct8x8(tb, C, false);
         haar_lanes<K>(tb, k, false);
         const float s2 = sigma * sigma;
         float n2 = 0.f;
@@ -171,26 +192,23 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) tz[i * 8 + j] = (float)__ldg(zimg + (int64_t)(cy + i) * W + cx + j);
-        dct8_rows(tz, C, false);
-        dct8_cols(tz, C, false);
+        dct8x8(tz, C, false);
         haar_lanes<K>(tz, k, false);
 #pragma unroll
         for (int e = 0; e < 64; ++e) tz[e] *= tb[e];
         haar_lanes<K>(tz, k, true);
-        dct8_cols(tz, C, true);
-        dct8_rows(tz, C, true);
+        dct8x8(tz, C, true);
         // aggregation of the group's real matches (slots < n_valid)
         if (live && k < nv) {
             if (regional) {
+                // numerator per pixel; the denominator sum w chi is the 8 x 8 box sum of the
+                // block weights placed at the blocks' top-left pixels (one add per block)
                 float* const pn = rnum + (cy - by0) * rw + (cx - bx0);
-                float* const pd = rden + (cy - by0) * rw + (cx - bx0);
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        atomicAdd(pn + i * rw + j, wgt * tz[i * 8 + j]);
-                        atomicAdd(pd + i * rw + j, wgt);
-                    }
+                    for (int j = 0; j < 8; ++j) atomicAdd(pn + i * rw + j, wgt * tz[i * 8 + j]);
+                atomicAdd(rwm + (cy - by0) * rw + (cx - bx0), wgt);
             } else {
                 float* const pn = num + b * plane + (int64_t)cy * W + cx;
                 float* const pd = den + b * plane + (int64_t)cy * W + cx;
@@ -206,8 +224,19 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
     }
     if (regional) {
         __syncthreads();
+        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) {  // horizontal 8-box of rwm
+            const int y = i / rw, x = i - y * rw;
+            float h = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h += x - j >= 0 ? rwm[y * rw + x - j] : 0.f;
+            rtmp[i] = h;
+        }
+        __syncthreads();
         for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) {
-            const float d = rden[i];
+            const int y = i / rw, x = i - y * rw;
+            float d = 0.f;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) d += y - t >= 0 ? rtmp[(y - t) * rw + x] : 0.f;
             if (d != 0.f) {
                 const int y = by0 + i / rw, x = bx0 + i % rw;
                 atomicAdd(num + b * plane + (int64_t)y * W + x, rnum[i]);
@@ -230,7 +259,7 @@ template <int K>
 cudaError_t launch_wiener(const int16_t* noisy, const float* basic, int B, int H, int W,
                           const int32_t* idx, const int32_t* nvalid, int Ry, int Rx,
                           const float* sigmas, float* num, float* den, cudaStream_t s) {
-    const int smem = 2 * REGION_MAX * 4;
+    const int smem = 3 * REGION_MAX * 4;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(wiener_tile_kernel<K>,
