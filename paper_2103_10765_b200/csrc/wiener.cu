@@ -11,14 +11,16 @@
 //   Y(x) = sum w U(x) / sum w chi(x) over the first n_valid blocks of every group (
 //   the pad blocks that fill short groups are left out).
 //
-// Mapping: one lane per block (K lanes per group, K a power of two <= 32): the block's 64
-// coefficients live in the lane's registers, the 2D DCT is two in-register passes of 8 x 8
-// products, the Haar transform along the group is a butterfly cascade across the K lanes
-// (shfl.xor; orthonormal, coefficients in the butterfly's positions, which the elementwise
-// shrinkage does not care about), and the weight's ||W||^2 is a K-lane reduction.  A CTA takes
-// an 8 x 8 tile of references; their blocks lie in the union of the tile's search windows, so
-// the aggregation sums go to a shared-memory copy of that region (bounding box of the tile's
-// blocks) and reach global memory as one atomic add per region pixel.  fp32 arithmetic.
+// Mapping: one lane per block (K lanes per group, K a power of two <= 32): the lane computes
+// its block's 2D DCT in registers (even/odd 8-point transforms) and writes the 64 coefficients
+// as one row of a per-warp shared buffer; read back by columns, each lane then holds one
+// (group, coefficient) column of K values and runs the Haar cascade, the shrinkage and the
+// inverse Haar in registers (coefficients in the cascade's in-place positions, which the
+// elementwise shrinkage does not care about); the rows go back to their lanes for the inverse
+// DCT.  ||W||^2 is a warp reduction of the per-column sums.  Aggregation: fire-and-forget fp32
+// reductions (RED) of w U into the numerator plane; the denominator sum w chi is the 8 x 8 box
+// sum of the block weights, so each block reduces its weight once at its top-left pixel and a
+// final tiled pass divides by the box sums.  fp32 arithmetic.
 #include <climits>
 #include <cstdint>
 
@@ -31,7 +33,9 @@ namespace {
 
 constexpr int WT = 8;                   // reference tile: WT x WT grid cells per CTA
 constexpr int WTHREADS = 128;
-constexpr int REGION_MAX = 6144;        // pixels of the shared aggregation region (3 x 24 KB)
+constexpr int TP = 65;                  // transpose buffer pitch (floats): conflict-free rows/columns
+constexpr int WARPS = WTHREADS / 32;
+constexpr int WIENER_SMEM = WARPS * 2 * 32 * TP * 4;
 
 // 8-point orthonormal DCT-II of v[0], v[st], .., v[7 st] in place, by the symmetry of its
 // rows: even rows see s_j = x_j + x_{7-j}, odd rows d_j = x_j - x_{7-j} (4 products each
@@ -86,24 +90,20 @@ __device__ __forceinline__ void dct8x8(float (&x)[64], const float* __restrict__
     }
 }
 
-// Orthonormal Haar cascade across the K lanes of a group (lane k = block k): at stride s only
-// the lanes holding approximation coefficients (k % s == 0) take part: k % 2s == 0 keeps
-// (x_k + x_{k+s}) / sqrt 2, k % 2s == s keeps (x_{k-s} - x_k) / sqrt 2 (a detail coefficient,
-// left alone from then on).  Forward runs s = 1, 2, .., K/2; the inverse runs the same butterfly
-// (its own inverse) in the reverse order.
+// Orthonormal Haar cascade of K values in registers, coefficients kept in the in-place lifting
+// positions (x[0] = scaling coefficient); the inverse undoes the levels in reverse order.
 template <int K>
-__device__ __forceinline__ void haar_lanes(float (&x)[64], int k, bool inverse) {
+__device__ __forceinline__ void haar_regs(float (&x)[K], bool inverse) {
     const float r2 = 0.70710678118654752f;
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
         const int s = inverse ? (K >> 1) >> t : 1 << t;
         if (s < 1 || s >= K) continue;
-        const bool act = (k & (s - 1)) == 0, lo = (k & s) == 0;
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-            const float p = __shfl_xor_sync(0xffffffffu, x[e], s);
-            const float y = lo ? (x[e] + p) * r2 : (p - x[e]) * r2;
-            x[e] = act ? y : x[e];
+        for (int i = 0; i < K; i += 2 * s) {
+            const float a = x[i], d = x[i + s];
+            x[i] = (a + d) * r2;
+            x[i + s] = (a - d) * r2;
         }
     }
 }
@@ -112,13 +112,12 @@ template <int K>
 __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         const int16_t* __restrict__ noisy, const float* __restrict__ basic, int H, int W,
         const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid, int Ry, int Rx,
-        const float* __restrict__ sigmas, float* __restrict__ num, float* __restrict__ den) {
+        const float* __restrict__ sigmas, float* __restrict__ num, float* __restrict__ wmap) {
     extern __shared__ float wsm[];
-    float* const rnum = wsm;                   // [REGION_MAX] numerator sums
-    float* const rwm = wsm + REGION_MAX;       // [REGION_MAX] block weights at block top-lefts
-    float* const rtmp = wsm + 2 * REGION_MAX;  // [REGION_MAX] horizontal box sums of rwm
+    // per warp: DCT coefficients of its 32 blocks (one row per block) for the basic estimate
+    // and the noisy image, transposed through shared memory for the Haar transform
+    float* const tbuf = wsm + (threadIdx.x >> 5) * 2 * 32 * TP;
     __shared__ float C[64];
-    __shared__ int bb[4];
     const int b = blockIdx.z;
     const int ty0 = blockIdx.y * WT, tx0 = blockIdx.x * WT;
     const int ny = min(WT, Ry - ty0), nx = min(WT, Rx - tx0);
@@ -131,26 +130,6 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         const float a = k == 0 ? 0.35355339059327376f : 0.5f;  // sqrt(1/8), sqrt(2/8)
         C[threadIdx.x] = a * cospif((float)((2 * i + 1) * k) / 16.0f);
     }
-    if (threadIdx.x == 0) { bb[0] = INT_MAX; bb[1] = -1; bb[2] = INT_MAX; bb[3] = -1; }
-    __syncthreads();
-    // bounding box of every block of the tile's groups
-    {
-        int y0 = INT_MAX, y1 = -1, x0 = INT_MAX, x1 = -1;
-        for (int q = threadIdx.x; q < ny * nx * K; q += WTHREADS) {
-            const int g = q / K, k = q - g * K;
-            const int gy = ty0 + g / nx, gx = tx0 + g % nx;
-            const int c = __ldg(idx + (((int64_t)b * Ry + gy) * Rx + gx) * K + k);
-            const int cy = c / W, cx = c - cy * W;
-            y0 = min(y0, cy); y1 = max(y1, cy); x0 = min(x0, cx); x1 = max(x1, cx);
-        }
-        atomicMin(&bb[0], y0); atomicMax(&bb[1], y1); atomicMin(&bb[2], x0); atomicMax(&bb[3], x1);
-    }
-    __syncthreads();
-    const int by0 = bb[0], bx0 = bb[2];
-    const int rh = bb[1] + 8 - by0, rw = bb[3] + 8 - bx0;
-    const bool regional = rh * rw <= REGION_MAX;
-    if (regional)
-        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) { rnum[i] = 0.f; rwm[i] = 0.f; }
     __syncthreads();
 
     constexpr int GPW = 32 / K;  // groups per warp pass
@@ -165,101 +144,132 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
         const int c = live ? __ldg(idx + ref * K + k) : 0;
         const int nv = live ? __ldg(nvalid + ref) : 0;
         const int cy = c / W, cx = c - cy * W;
-        // basic-estimate group -> T_B -> shrinkage W (kept in tb)
-        float tb[64];
+        // 2D DCT of this lane's block, basic estimate and noisy image, into the warp's rows
+        {
+            float blk[64];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) tb[i * 8 + j] = __ldg(bimg + (int64_t)(cy + i) * W + cx + j);
-        dct8x8(tb, C, false);
-        haar_lanes<K>(tb, k, false);
+                for (int j = 0; j < 8; ++j) blk[i * 8 + j] = __ldg(bimg + (int64_t)(cy + i) * W + cx + j);
+            dct8x8(blk, C, false);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) tbuf[lane * TP + e] = blk[e];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    blk[i * 8 + j] = (float)__ldg(zimg + (int64_t)(cy + i) * W + cx + j);
+            dct8x8(blk, C, false);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) tbuf[(32 + lane) * TP + e] = blk[e];
+        }
+        __syncwarp();
+        // Haar along each group, one (group, coefficient) column of K values per lane and pass:
+        // shrinkage from the basic column, applied to the noisy column, inverse Haar in place
         const float s2 = sigma * sigma;
+        float n2g[GPW];
+#pragma unroll
+        for (int q = 0; q < GPW; ++q) n2g[q] = 0.f;
+#pragma unroll
+        for (int pass = 0; pass < 2 * GPW; ++pass) {
+            const int col = lane + 32 * pass;     // 0 .. 64 GPW - 1
+            const int qg = col >> 6, e = col & 63;  // group slot, coefficient
+            float tb[K], tz[K];
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                tb[kk] = tbuf[(qg * K + kk) * TP + e];
+                tz[kk] = tbuf[(32 + qg * K + kk) * TP + e];
+            }
+            haar_regs<K>(tb, false);
+            haar_regs<K>(tz, false);
+            float n2 = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                const float t2 = tb[kk] * tb[kk];
+                const float dn = t2 + s2;
+                const float wv = dn > 0.f ? t2 / dn : 1.f;
+                n2 = fmaf(wv, wv, n2);
+                tz[kk] *= wv;
+            }
+#pragma unroll
+            for (int q = 0; q < GPW; ++q) n2g[q] += q == qg ? n2 : 0.f;
+            haar_regs<K>(tz, true);
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) tbuf[(32 + qg * K + kk) * TP + e] = tz[kk];
+        }
+        // ||W||^2 of this lane's group: sum over the warp of the partial sums for slot gslot
         float n2 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-            const float t2 = tb[e] * tb[e];
-            const float dn = t2 + s2;
-            const float wv = dn > 0.f ? t2 / dn : 1.f;
-            tb[e] = wv;
-            n2 = fmaf(wv, wv, n2);
-        }
+        for (int q = 0; q < GPW; ++q) {
+            float v = n2g[q];
 #pragma unroll
-        for (int o = 1; o < K; o <<= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            n2 += q == gslot ? v : 0.f;
+        }
         const float wgt = (sigma > 0.f && n2 > 0.f) ? 1.f / (s2 * n2) : 1.f;
-        // noisy group -> T_Z, shrink, inverse
+        __syncwarp();
         float tz[64];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) tz[i * 8 + j] = (float)__ldg(zimg + (int64_t)(cy + i) * W + cx + j);
-        dct8x8(tz, C, false);
-        haar_lanes<K>(tz, k, false);
-#pragma unroll
-        for (int e = 0; e < 64; ++e) tz[e] *= tb[e];
-        haar_lanes<K>(tz, k, true);
+        for (int e = 0; e < 64; ++e) tz[e] = tbuf[(32 + lane) * TP + e];
+        __syncwarp();  // the buffer is rewritten by the next pass of the loop
         dct8x8(tz, C, true);
-        // aggregation of the group's real matches (slots < n_valid)
+        // aggregation of the group's real matches (slots < n_valid): the
+        // numerator per pixel (fire-and-forget fp32 reductions in L2); the denominator
+        // sum w chi is the 8 x 8 box sum of the block weights, so each block adds its weight
+        // once, at its top-left pixel, and the final pass takes the box sums
         if (live && k < nv) {
-            if (regional) {
-                // numerator per pixel; the denominator sum w chi is the 8 x 8 box sum of the
-                // block weights placed at the blocks' top-left pixels (one add per block)
-                float* const pn = rnum + (cy - by0) * rw + (cx - bx0);
+            float* const pn = num + b * plane + (int64_t)cy * W + cx;
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) atomicAdd(pn + i * rw + j, wgt * tz[i * 8 + j]);
-                atomicAdd(rwm + (cy - by0) * rw + (cx - bx0), wgt);
-            } else {
-                float* const pn = num + b * plane + (int64_t)cy * W + cx;
-                float* const pd = den + b * plane + (int64_t)cy * W + cx;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        atomicAdd(pn + (int64_t)i * W + j, wgt * tz[i * 8 + j]);
-                        atomicAdd(pd + (int64_t)i * W + j, wgt);
-                    }
-            }
-        }
-    }
-    if (regional) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) {  // horizontal 8-box of rwm
-            const int y = i / rw, x = i - y * rw;
-            float h = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) h += x - j >= 0 ? rwm[y * rw + x - j] : 0.f;
-            rtmp[i] = h;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < rh * rw; i += WTHREADS) {
-            const int y = i / rw, x = i - y * rw;
-            float d = 0.f;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) d += y - t >= 0 ? rtmp[(y - t) * rw + x] : 0.f;
-            if (d != 0.f) {
-                const int y = by0 + i / rw, x = bx0 + i % rw;
-                atomicAdd(num + b * plane + (int64_t)y * W + x, rnum[i]);
-                atomicAdd(den + b * plane + (int64_t)y * W + x, d);
-            }
+                for (int j = 0; j < 8; ++j) atomicAdd(pn + (int64_t)i * W + j, wgt * tz[i * 8 + j]);
+            atomicAdd(wmap + b * plane + (int64_t)cy * W + cx, wgt);
         }
     }
 }
 
-__global__ void wiener_divide_kernel(const float* __restrict__ num, const float* __restrict__ den,
-                                     float* __restrict__ out, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float d = den[i];
-        out[i] = d > 0.f ? num[i] / d : 0.f;
+// out = num / den with den(y, x) = sum of the block weights whose top-left lies in
+// [y-7, y] x [x-7, x]: 32 x 32 output tiles, the weight map staged with its 7-pixel halo.
+__global__ void __launch_bounds__(256) wiener_divide_kernel(const float* __restrict__ num,
+                                                            const float* __restrict__ wmap,
+                                                            float* __restrict__ out, int H, int W) {
+    __shared__ float m[39][40];
+    __shared__ float hs[39][33];
+    const int b = blockIdx.z;
+    const int y0 = blockIdx.y * 32, x0 = blockIdx.x * 32;
+    const int64_t plane = (int64_t)H * W;
+    const float* __restrict__ wm = wmap + b * plane;
+    for (int i = threadIdx.x; i < 39 * 39; i += 256) {
+        const int r = i / 39, c = i - r * 39;
+        const int y = y0 - 7 + r, x = x0 - 7 + c;
+        m[r][c] = (y >= 0 && y < H && x >= 0 && x < W) ? wm[(int64_t)y * W + x] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 39 * 32; i += 256) {
+        const int r = i >> 5, c = i & 31;
+        float h = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h += m[r][c + j];
+        hs[r][c] = h;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+        const int r = i >> 5, c = i & 31;
+        const int y = y0 + r, x = x0 + c;
+        if (y >= H || x >= W) continue;
+        float d = 0.f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) d += hs[r + t][c];
+        const int64_t o = b * plane + (int64_t)y * W + x;
+        out[o] = d > 0.f ? num[o] / d : 0.f;
     }
 }
 
 template <int K>
 cudaError_t launch_wiener(const int16_t* noisy, const float* basic, int B, int H, int W,
                           const int32_t* idx, const int32_t* nvalid, int Ry, int Rx,
-                          const float* sigmas, float* num, float* den, cudaStream_t s) {
-    const int smem = 3 * REGION_MAX * 4;
+                          const float* sigmas, float* num, float* wmap, cudaStream_t s) {
+    const int smem = WIENER_SMEM;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(wiener_tile_kernel<K>,
@@ -269,7 +279,7 @@ cudaError_t launch_wiener(const int16_t* noisy, const float* basic, int B, int H
     }
     dim3 grid((unsigned)((Rx + WT - 1) / WT), (unsigned)((Ry + WT - 1) / WT), (unsigned)B);
     wiener_tile_kernel<K><<<grid, WTHREADS, smem, s>>>(noisy, basic, H, W, idx, nvalid, Ry, Rx,
-                                                       sigmas, num, den);
+                                                       sigmas, num, wmap);
     return cudaGetLastError();
 }
 
@@ -307,8 +317,7 @@ extern "C" int gbm3d_wiener_stage2(const int16_t* noisy, const float* basic, int
         default: e = launch_wiener<32>(noisy, basic, B, H, W, idx, n_valid, Ry, Rx, sigmas, num, den, s); break;
     }
     if (e != cudaSuccess) return GBM3D_ERR_CUDA;
-    const int64_t n = (int64_t)B * H * W;
-    const int64_t blocks = (n + 255) / 256;
-    wiener_divide_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(num, den, out, n);
+    dim3 dgrid((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), (unsigned)B);
+    wiener_divide_kernel<<<dgrid, 256, 0, s>>>(num, den, out, H, W);
     return cudaGetLastError() == cudaSuccess ? GBM3D_OK : GBM3D_ERR_CUDA;
 }
