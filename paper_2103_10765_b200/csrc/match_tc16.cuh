@@ -35,17 +35,9 @@ constexpr int TY = 16, TX = 8;
 constexpr int NB = 64;           // candidate columns per MMA tile (N)
 constexpr int PCH = 72;          // fp16 plane pitch in elements (64 + 7 + pad)
 constexpr int NTS = 8;           // TMEM stages (64 columns each)
-#ifndef GBM3D_TC16_NSEL
-#define GBM3D_TC16_NSEL 1
-#endif
-constexpr int NSEL = GBM3D_TC16_NSEL;  // selector warps per lane quarter (rows alternate)
-constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 4 + 4 * NSEL;
+constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8;  // epilogue w, selector 4 + w, MMA
 constexpr int THREADS = 32 * (MMA_WARP + 1);
-#ifndef GBM3D_TC16_NSLOT
-#define GBM3D_TC16_NSLOT 2
-#endif
-constexpr int NSLOT = GBM3D_TC16_NSLOT;  // staged rows per lane quarter (a multiple of NSEL)
-static_assert(NSLOT % NSEL == 0, "each selector owns NSLOT / NSEL staging slots");
+constexpr int NSLOT = 2;         // staged rows per lane quarter (epilogue one row ahead)
 constexpr int STG_PITCH = 68;    // words per lane and staged row: u[64], mask lo/hi, gate, row
 constexpr int A_BYTES = 128 * 128;
 constexpr int XP = (NB / 8) * 128;  // bytes per pre-shifted plane row (8 chunks of 8 x 16 B)
@@ -71,10 +63,10 @@ struct Tc16Geom {
         g.off_nc = g.off_x + g.PR * XP;
         g.off_stg = g.off_nc + g.NT * NB * 4;  // raw tile, fp16 plane, squares before the loop
         g.off_bar = g.off_stg + EPI_WARPS * NSLOT * 32 * STG_PITCH * 4;
-        // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT]; gates[NSEL][128],
-        // consumed[EPI_WARPS][NSEL], range scratch[2], TMEM address
+        // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT]; gates[128], consumed[EPI_WARPS],
+        // range scratch[2], TMEM address
         g.total = g.off_bar + (2 * NTS + 2 * EPI_WARPS * NSLOT) * 8 +
-                  (NSEL * EPI_WARPS * 32 + EPI_WARPS * NSEL + 2 + 1) * 4 + 16;
+                  (EPI_WARPS * 32 + EPI_WARPS + 2 + 1) * 4 + 16;
         return g;
     }
 };
@@ -226,8 +218,8 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     uint64_t* const sempty = sfull + EPI_WARPS * NSLOT;
     volatile int* const gate_pub = reinterpret_cast<volatile int*>(sempty + EPI_WARPS * NSLOT);
     // rows taken by selector (w, h)
-    volatile int* const consumed = gate_pub + NSEL * EPI_WARPS * 32;
-    int* const rng = const_cast<int*>(consumed + EPI_WARPS * NSEL);  // tile min, max
+    volatile int* const consumed = gate_pub + EPI_WARPS * 32;    // rows taken by selector w
+    int* const rng = const_cast<int*>(consumed + EPI_WARPS);     // tile min, max
     uint32_t* const tslot = reinterpret_cast<uint32_t*>(rng + 2);
 
     const int t_lo = max(0, -gy0), t_hi = min(g.NT - 1, (p.H - P) - gy0);
@@ -334,8 +326,8 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             tc::fence_mbar_init();
         }
         if (warp == MMA_WARP) tc::tmem_alloc<TMEM_COLS>(tslot);
-        if (threadIdx.x < NSEL * EPI_WARPS * 32) gate_pub[threadIdx.x] = p.tdr0 + 1;
-        if (threadIdx.x < EPI_WARPS * NSEL) consumed[threadIdx.x] = 0;
+        if (threadIdx.x < EPI_WARPS * 32) gate_pub[threadIdx.x] = p.tdr0 + 1;
+        if (threadIdx.x < EPI_WARPS) consumed[threadIdx.x] = 0;
         __syncthreads();  // centred raw values and the fp16 plane complete
         if (threadIdx.x == 0) TC_TR(4, clock64());
         // horizontal P-sums of squares hs[y][n] (n < 64), 8 columns per item (sliding sum)
@@ -428,8 +420,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
         __syncwarp();
     } else {
         const bool is_sel = warp >= SEL_WARP0;
-        const int w = is_sel ? (warp - SEL_WARP0) & 3 : warp;
-        const int hsel = is_sel ? (warp - SEL_WARP0) >> 2 : 0;  // this selector's row parity
+        const int w = is_sel ? warp - SEL_WARP0 : warp;
         const int a = 4 * w + (lane >> 3), bb = lane & 7;
         const bool refok = (ky0 + a < kr1) && (kx0 + bb < p.Rx_reg) && (p.K > 1);
         const int ty = r + S * a, tx = r + S * bb;
@@ -464,23 +455,11 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 if (used >= NSLOT) tc::mbar_wait(&sempty[w * NSLOT + slot], ((used / NSLOT) - 1) & 1);
                 // while the lists fill (gates still at their start value) stage one row at a
                 // time: a row staged against an unset gate passes its whole window
-                // (the selectors' lists each hold K-1 keys below their own top, so the smallest
-                // published top bounds the final (K-1)-th key: every selector may gate with it)
-                auto read_gate = [&]() {
-                    int gt = gate_pub[w * 32 + lane];
-#pragma unroll
-                    for (int h = 1; h < NSEL; ++h) gt = min(gt, gate_pub[h * EPI_WARPS * 32 + w * 32 + lane]);
-                    return gt;
-                };
-                int gate = read_gate();
+                int gate = gate_pub[w * 32 + lane];
                 if (used > 0 && __any_sync(0xffffffffu, gate == gate0 && refok)) {
-                    for (;;) {
-                        int c = 0;
-#pragma unroll
-                        for (int h = 0; h < NSEL; ++h) c += consumed[w * NSEL + h];
-                        if (c >= used) break;
+                    while (consumed[w] < used) {
                     }
-                    gate = read_gate();
+                    gate = gate_pub[w * 32 + lane];
                 }
                 // u = N_q - 2 <f_p, f_q> passes iff u < T = gate - N_p; stage v = u - T (exact for
                 // every passing candidate, sign-correct for the rest): d = v + gate
@@ -547,7 +526,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             // d + 2^23 as an fp32 bit pattern is 0x4B000000 + d (exact for d < 2^23), and
             // 0x4B000000 << cb == 0 (mod 2^32) for cb >= 8: key = bits(v + gate + 2^23) << cb | code
             const uint32_t kmul = 1u << cb;
-            for (used = hsel; used < nrel; used += NSEL) {
+            for (used = 0; used < nrel; ++used) {
                 const int slot = used % NSLOT;
                 if (lane == 0) TC_TR(5000 + w * 200 + used, clock64());
                 tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
@@ -620,34 +599,11 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
                 if (lane == 0) TC_TR(3000 + w * 200 + used, clock64());
                 if (lane == 0) TC_TR(4000 + w * 200 + used, R);
                 const uint32_t top = L[KL - 1];
-                gate_pub[hsel * EPI_WARPS * 32 + w * 32 + lane] =
+                gate_pub[w * 32 + lane] =
                     ((top == KEY_INF) ? p.tdr0 : min((int)(top >> cb), p.tdr0)) + 1;
                 __syncwarp();
-                if (lane == 0) consumed[w * NSEL + hsel] = used / NSEL + 1;
+                if (lane == 0) consumed[w] = used + 1;
             }
-            if constexpr (NSEL > 1) {
-                // merge: selector h > 0 leaves its sorted list in its last staging slot (all rows
-                // consumed), selector 0 inserts the keys below its own top
-                uint32_t* const mine = stg0 + (NSLOT - NSEL + hsel) * 32 * STG_PITCH;
-                if (hsel > 0) {
-#pragma unroll
-                    for (int i = 0; i < KL; ++i) mine[i] = L[i];
-                }
-                asm volatile("bar.sync %0, %1;" ::"r"(1 + w), "r"(32 * NSEL) : "memory");
-#pragma unroll 1
-                for (int h = 1; hsel == 0 && h < NSEL; ++h) {
-                    const uint32_t* const other = stg0 + (NSLOT - NSEL + h) * 32 * STG_PITCH;
-#pragma unroll 1
-                    for (int i = 0; i < KL; ++i) {
-                        const uint32_t x = other[i];
-                        if (!__any_sync(0xffffffffu, x < L[KL - 1])) break;
-                        list_insert<KP>(L, x);
-                    }
-                }
-                __syncwarp();
-            }
-
-            if (hsel == 0) {
             if (threadIdx.x == 32 * SEL_WARP0) TC_TR(7, clock64());
             // ---- output: slot 0 = self, ranks 1.. = list, pads (self, -1); coalesced rows
             const int Kout = p.K;
@@ -756,7 +712,6 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             if (refok && p.nvalid) {
                 const int64_t ref = ref0 + (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
                 p.nvalid[ref] = 1 + cnt;
-            }
             }
         }
     }
