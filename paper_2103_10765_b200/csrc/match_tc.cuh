@@ -33,6 +33,29 @@ namespace gbm3d {
 
 #if GBM3D_TC_TRACE  // dev-only timeline of one CTA (clock64), read by gbm3d_dev_tc_trace
 static __device__ long long g_tc_trace[8192];
+// dev-only: per CTA (linear block id) start / end %globaltimer and SM id
+static __device__ long long g_cta_span[65536][3];
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int smid() {
+    int s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
+#define TC_SPAN(k, v)                                                                      \
+    do {                                                                                   \
+        const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;   \
+        if (cta < 65536) g_cta_span[cta][k] = (v);                                         \
+    } while (0)
+#else
+#define TC_SPAN(k, v) \
+    do {              \
+    } while (0)
+#endif
+#if GBM3D_TC_TRACE
 #define TC_TR(i, v)                                                                   \
     do {                                                                              \
         if (blockIdx.x == 10 && blockIdx.y == 10 && blockIdx.z == 0) g_tc_trace[i] = (v); \

@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     using namespace tc16;
     extern __shared__ __align__(1024) unsigned char sm[];
     if (threadIdx.x == 0) TC_TR(2, clock64());
+    if (threadIdx.x == 0) { TC_SPAN(0, gtimer()); TC_SPAN(2, (long long)smid()); }
     const Tc16Geom g = Tc16Geom::make(S, p.r);
     constexpr int P = 8;
     const int r = p.r;
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     tc::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) TC_TR(1, clock64());
+    if (threadIdx.x == 0) TC_SPAN(1, gtimer());
     if (warp == MMA_WARP) {
         tc::tc_fence_after();
         tc::tmem_dealloc<tc16::TMEM_COLS>(tmem);
