@@ -1,0 +1,167 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY.  Stage-1 global volume hard thresholding of G-BM3D
+(SURVEY.md 8f-4), float64, written step by step in the paper's order.
+
+PAPER.md:132-149 (section "Global Volume Hard Thresholding") and :154-206 (formal details):
+  V      the volume of matched blocks of the tiling references (slice 0 = Z),
+  U_h    = S_-h T3D^-1( Upsilon( T3D( S_h V ) ) ),
+  U      = (1/H) sum_h U_h, H = 2, h = 0, 1,
+  w_pq   = 1 / TV(U_pq),
+  Y(x)   = sum w_pq U_pq^x(x) / sum w_pq chi_x(x)        (PAPER.md:190; pads left out, :142).
+Parameters: 2D biorthogonal 1.5 wavelets in space, Haar along the group,
+3 levels, hard thresholds lambda_l = sigma (3.6 - 0.3 l).  Readings S1-S7 in DESIGN.md.
+
+Only tests/ use this; the CUDA path shares no code with it.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+import oracle
+
+# bior1.5 (Cohen-Daubechies-Feauveau, box synthesis scaling function): analysis lowpass on
+# n = -4..5, synthesis lowpass = Haar on n = 0, 1; highpasses by the biorthogonal QMF relations
+# g~[n] = (-1)^n h[1-n] (analysis), g[n] = (-1)^n h~[1-n] (synthesis).
+_S2 = math.sqrt(2.0)
+H_AN = {n: v * _S2 / 256.0 for n, v in zip(range(-4, 6), (3, -3, -22, 22, 128, 128, 22, -22, -3, 3))}
+H_SY = {0: 1.0 / _S2, 1: 1.0 / _S2}
+G_AN = {n: ((-1) ** n) * H_SY.get(1 - n, 0.0) for n in range(0, 2)}
+G_SY = {n: ((-1) ** n) * H_AN.get(1 - n, 0.0) for n in range(-4, 6)}
+
+
+def dwt1(x: np.ndarray, axis: int):
+    """One analysis level along `axis`, periodic: a[k] = sum_n h~[n] x[2k+n],
+    d[k] = sum_n g~[n] x[2k+n] (indices mod the length)."""
+    x = np.moveaxis(np.asarray(x, dtype=np.float64), axis, 0)
+    M = x.shape[0]
+    k = np.arange(M // 2)
+    a = sum(v * x[(2 * k + n) % M] for n, v in H_AN.items())
+    d = sum(v * x[(2 * k + n) % M] for n, v in G_AN.items())
+    return np.moveaxis(a, 0, axis), np.moveaxis(d, 0, axis)
+
+
+def idwt1(a: np.ndarray, d: np.ndarray, axis: int) -> np.ndarray:
+    """Synthesis: x[2k+n] += h[n] a[k] + g[n] d[k] (periodic)."""
+    a = np.moveaxis(np.asarray(a, dtype=np.float64), axis, 0)
+    d = np.moveaxis(np.asarray(d, dtype=np.float64), axis, 0)
+    half = a.shape[0]
+    M = 2 * half
+    x = np.zeros((M,) + a.shape[1:])
+    for k in range(half):
+        for n, v in H_SY.items():
+            x[(2 * k + n) % M] += v * a[k]
+        for n, v in G_SY.items():
+            x[(2 * k + n) % M] += v * d[k]
+    return np.moveaxis(x, 0, axis)
+
+
+def dwt2(img: np.ndarray, levels: int):
+    """2D separable transform of the last two axes (rows then columns of the current LL band,
+    Mallat), returned in the usual in-place layout: at level l the LL band of size (H/2^l,
+    W/2^l) sits in the top-left corner, its details LH (top-right), HL (bottom-left), HH."""
+    out = np.array(img, dtype=np.float64)
+    h, w = out.shape[-2:]
+    for _ in range(levels):
+        band = out[..., :h, :w]
+        a, d = dwt1(band, -1)               # along x
+        lo = np.concatenate([a, d], axis=-1)
+        a2, d2 = dwt1(lo, -2)               # along y
+        out[..., :h, :w] = np.concatenate([a2, d2], axis=-2)
+        h //= 2
+        w //= 2
+    return out
+
+
+def idwt2(coef: np.ndarray, levels: int) -> np.ndarray:
+    out = np.array(coef, dtype=np.float64)
+    H, W = out.shape[-2:]
+    for lev in range(levels, 0, -1):
+        h, w = H >> (lev - 1), W >> (lev - 1)
+        band = out[..., :h, :w]
+        lo = idwt1(band[..., : h // 2, :], band[..., h // 2:, :], -2)
+        out[..., :h, :w] = idwt1(lo[..., : w // 2], lo[..., w // 2:], -1)
+    return out
+
+
+def haar_z(V: np.ndarray, levels: int, inverse: bool = False) -> np.ndarray:
+    """Orthonormal Haar along axis 0 with `levels` cascade levels, in-place lifting positions
+    (level with stride s pairs entries i and i + s for i a multiple of 2s)."""
+    X = np.array(V, dtype=np.float64)
+    K = X.shape[0]
+    strides = [1 << t for t in range(levels)]
+    for s in (reversed(strides) if inverse else strides):
+        for i in range(0, K, 2 * s):
+            a, d = X[i].copy(), X[i + s].copy()
+            X[i] = (a + d) / _S2
+            X[i + s] = (a - d) / _S2
+    return X
+
+
+def spatial_level_map(H: int, W: int, levels: int) -> np.ndarray:
+    """Level of every position of the in-place 2D layout: 1..L for the detail bands, L for the
+    final LL band (reading S2), as an int array [H, W]."""
+    lev = np.full((H, W), levels, dtype=np.int64)
+    h, w = H, W
+    for l in range(1, levels + 1):
+        lev[:h, :w] = l
+        h //= 2
+        w //= 2
+    lev[:h, :w] = levels  # LL_L
+    return lev
+
+
+def w3d_threshold(V: np.ndarray, sigma: float, levels: int) -> np.ndarray:
+    """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2)."""
+    K, H, W = V.shape
+    lz = min(levels, int(math.log2(K)))
+    T = haar_z(dwt2(V, levels), lz)
+    lev = spatial_level_map(H, W, levels)
+    lam = sigma * (3.6 - 0.3 * lev)
+    keep = np.abs(T) >= lam[None]                        # Upsilon
+    # the coefficients that are approximations in space (LL_L) and along z are kept (S2)
+    hL, wL = H >> levels, W >> levels
+    zapprox = np.zeros(K, dtype=bool)
+    zapprox[:: 1 << lz] = True
+    keep[np.ix_(zapprox, np.arange(hL), np.arange(wL))] = True
+    return idwt2(haar_z(np.where(keep, T, 0.0), lz, inverse=True), levels)
+
+
+def filter_volume(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)) -> np.ndarray:
+    """U = (1/H) sum_h S_-h( T3D^-1 Upsilon T3D (S_h V) ), S_h = circular shift by h along all
+    three axes (reading S3)."""
+    acc = np.zeros(V.shape)
+    for h in shifts:
+        Vh = np.roll(V, (h, h, h), axis=(0, 1, 2))
+        acc += np.roll(w3d_threshold(Vh, sigma, levels), (-h, -h, -h), axis=(0, 1, 2))
+    return acc / len(shifts)
+
+
+def tv3d(G: np.ndarray) -> float:
+    """Anisotropic 3D total variation of a group [K, N, N]: sum of |forward differences| along
+    the group axis and both block axes (reading S4)."""
+    return float(np.abs(np.diff(G, axis=0)).sum() + np.abs(np.diff(G, axis=1)).sum()
+                 + np.abs(np.diff(G, axis=2)).sum())
+
+
+def stage1(noisy: np.ndarray, idx: np.ndarray, n_valid: np.ndarray, patch: int, sigma: float,
+           levels: int = 3, shifts=(0, 1)) -> np.ndarray:
+    """phi(Z) for tiling references (stride = N): the filtered volume's groups are aggregated
+    at their blocks' positions with weights 1 / TV, first n_valid blocks."""
+    H, W = noisy.shape
+    N = patch
+    V = oracle.gather_volume(noisy, idx, N).astype(np.float64)   # [K, H, W]
+    U = filter_volume(V, sigma, levels, shifts)
+    Ry, Rx, K = idx.shape
+    num = np.zeros((H, W))
+    den = np.zeros((H, W))
+    for p in range(Ry):
+        for q in range(Rx):
+            G = U[:, p * N:(p + 1) * N, q * N:(q + 1) * N]
+            tv = tv3d(G)
+            w = 1.0 / tv if tv > 0 else 1.0
+            for k in range(int(n_valid[p, q])):
+                cy, cx = divmod(int(idx[p, q, k]), W)
+                num[cy:cy + N, cx:cx + N] += w * G[k]
+                den[cy:cy + N, cx:cx + N] += w
+    return num / den
