@@ -294,6 +294,7 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
     }
     line["gather"] = run_gather(args, cfg, call, torch, g, img, outs[0], flush_buf)
     line["wiener"] = run_wiener(args, cfg, call, torch, g, img, outs, flush_buf)
+    line["stage1"] = run_stage1(args, cfg, call, torch, g, img, flush_buf)
     if want_e2e:
         line["e2e"] = run_e2e(args, cfg, call, torch, g)
     if want_cpu:
@@ -375,6 +376,51 @@ def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
                          "peak_basis": "64 FFMA lanes/clk/SM x 2 x 148 SMs x 1965 MHz"}}
 
 
+def run_stage1(args, cfg, call, torch, g, img, flush_buf):
+    """stage-1 global volume hard thresholding of the workload's image(s) with
+    tiling references (stride = patch = 8, K = 16, the paper's K), matching included in the
+    tables but not in the timing.  HBM roofline: ~28 streaming passes over the K x H x W fp32
+    volume (per spin and level: analysis x/y, z pass, synthesis y/x; plus build, TV,
+    aggregation), counted in DESIGN.md."""
+    N, K, levels = 8, 16, 3
+    if cfg.H % 16 or cfg.W % 16:
+        return None
+    idx, dist, nv = g.block_match(img, N, N, call.radius, K, None, check=False)
+    sig = list(cfg_sigmas(cfg))
+    out = torch.empty(img.shape, dtype=torch.float32, device=img.device)
+    ws = torch.empty(g.load_library().gbm3d_stage1_workspace_bytes(cfg.B, cfg.H, cfg.W, N, K),
+                     dtype=torch.uint8, device=img.device)
+
+    def step():
+        g.stage1_denoise(img, idx, nv, N, sig, levels, out=out, workspace=ws)
+
+    times = measure_device(step, args.steps, args.warmup, flush_buf.zero_, torch, soak_s=0.2)
+    ms = statistics.mean(times)
+    vol = cfg.B * K * cfg.H * cfg.W * 4
+    # per spin: analysis and synthesis each read + write the level-l band twice (x and y
+    # passes: 4 vol / 4^l), the z pass reads + writes once (2 vol); two spins; plus the volume
+    # build (1), TV (1), aggregation (1) and the accumulator read-modify-write (1)
+    passes = 2 * (2 * sum(4 / 4 ** l for l in range(levels)) + 2) + 4
+    nbytes = passes * vol
+    peak, src = measured_peak("hbm_gbs", 7672.0)
+    ach = nbytes / (ms * 1e-3) / 1e9
+    del out, ws
+    return {"what": "gbm3d_stage1_denoise: bior1.5 x Haar global volume hard thresholding, 2 cycle "
+                    "spins, 1/TV weights, aggregation (tiling refs N=8, K=16)",
+            "ms": ms, "pixels_per_s": cfg.B * cfg.H * cfg.W / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "bytes_per_call": nbytes, "peak_source": src}}
+
+
+def cfg_sigmas(cfg):
+    from synth import make_image
+    if cfg.sigma is not None:
+        return [cfg.sigma] * cfg.B
+    # per-image sigma of the recipe (drawn by the generator)
+    return [make_image(cfg.H, cfg.W, cfg.n_rect, cfg.n_tex, None, s, return_clean=True)[2]
+            for s in list(cfg.seeds)[:cfg.B]]
+
+
 def run_e2e(args, cfg, call, torch, g):
     """Same metric through the host-buffer C-ABI entry: pinned H2D of the images, the match,
     D2H of idx/dist/n_valid, all inside each timed step."""
@@ -446,7 +492,7 @@ def main():
                                                     "gevals_per_s", "roofline",
                                                     "roofline_tensor", "e2e", "config",
                                                     "clocks", "gpu_launches", "gather",
-                                                    "wiener")}}
+                                                    "wiener", "stage1")}}
     print(json.dumps(line), flush=True)
 
 

@@ -157,6 +157,28 @@ int gbm3d_wiener_stage2(const int16_t* noisy, const float* basic, int B, int H, 
                         const float* sigmas, float* out, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* ---- Stage-1 global volume hard thresholding, the
+ * operator phi of PAPER.md:200-204 for one noisy image per batch entry.  References tile the
+ * image (stride = patch = N; H and W multiples of N and of 2^(levels+1)); idx / n_valid are the
+ * tables of gbm3d_block_match* for that grid (K a power of two <= 32).  The volume of matched
+ * blocks V (slice 0 = Z) is transformed by a 3D wavelet transform -- 2D bior1.5 over (y, x),
+ * periodic, `levels` Mallat levels (the paper uses 3), then Haar along the group with
+ * min(levels, log2 K) levels -- hard thresholded with lambda_l = sigma (3.6 - 0.3 l) by spatial
+ * level (the coarsest approximation kept), inverted, averaged over the cycle spins h = 0, 1
+ * (circular shifts of V by h along all three axes), and aggregated with the group weights
+ * 1 / TV(U_pq) (anisotropic 3D total variation), pad blocks left out.
+ * noisy: device int16 [B][H][W]; sigmas: device float32 [B]; out: device float32 [B][H][W];
+ * workspace: gbm3d_stage1_workspace_bytes(B, H, W, patch, K) bytes (4 float volumes + 2 planes).
+ * fp32 with atomic accumulation: matches a float64 evaluation within DESIGN.md's tolerance.
+ * The translation trials of PAPER.md:203 (match and filter circularly shifted images, shift
+ * back, average) are the caller's: each trial is a gbm3d_block_match + gbm3d_stage1_denoise.
+ * Errors: GBM3D_ERR_ARG (null pointers, sizes, small workspace), GBM3D_ERR_UNSUPPORTED (K not a
+ * power of two or > 32, patch > 16, levels > 5), GBM3D_ERR_CUDA. */
+size_t gbm3d_stage1_workspace_bytes(int B, int H, int W, int patch, int K);
+int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch, const int32_t* idx,
+                         const int32_t* n_valid, int K, const float* sigmas, int levels, float* out,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
  * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,

@@ -111,13 +111,14 @@ def spatial_level_map(H: int, W: int, levels: int) -> np.ndarray:
     return lev
 
 
-def w3d_threshold(V: np.ndarray, sigma: float, levels: int) -> np.ndarray:
-    """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2)."""
+def w3d_threshold(V: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
+    """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2).  `lam_scale`
+    (tests only) scales the thresholds, to find the decisions that sit within rounding of them."""
     K, H, W = V.shape
     lz = min(levels, int(math.log2(K)))
     T = haar_z(dwt2(V, levels), lz)
     lev = spatial_level_map(H, W, levels)
-    lam = sigma * (3.6 - 0.3 * lev)                     # PAPER.md:241
+    lam = lam_scale * sigma * (3.6 - 0.3 * lev)         # PAPER.md:241
     keep = np.abs(T) >= lam[None]                        # Upsilon, PAPER.md:173-178
     # the coefficients that are approximations in space (LL_L) and along z are kept (S2)
     hL, wL = H >> levels, W >> levels
@@ -127,13 +128,32 @@ def w3d_threshold(V: np.ndarray, sigma: float, levels: int) -> np.ndarray:
     return idwt2(haar_z(np.where(keep, T, 0.0), lz, inverse=True), levels)
 
 
-def filter_volume(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)) -> np.ndarray:
+def threshold_margin(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)) -> float:
+    """Tests only: the smallest relative distance | |alpha| - lambda | / lambda over every
+    thresholded coefficient of every cycle spin -- the precision a second implementation needs
+    to take all of Upsilon's keep/zero decisions the same way."""
+    K, H, W = V.shape
+    lz = min(levels, int(math.log2(K)))
+    lev = spatial_level_map(H, W, levels)
+    lam = sigma * (3.6 - 0.3 * lev)
+    best = math.inf
+    for h in shifts:
+        T = haar_z(dwt2(np.roll(V, (h, h, h), axis=(0, 1, 2)), levels), lz)
+        rel = np.abs(np.abs(T) - lam[None]) / lam[None]
+        hL, wL = H >> levels, W >> levels
+        rel[:: 1 << lz, :hL, :wL] = np.inf  # always kept
+        best = min(best, float(rel.min()))
+    return best
+
+
+def filter_volume(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1),
+                  lam_scale: float = 1.0) -> np.ndarray:
     """U = (1/H) sum_h S_-h( T3D^-1 Upsilon T3D (S_h V) ), S_h = circular shift by h along all
     three axes (reading S3)."""
     acc = np.zeros(V.shape)
     for h in shifts:
         Vh = np.roll(V, (h, h, h), axis=(0, 1, 2))
-        acc += np.roll(w3d_threshold(Vh, sigma, levels), (-h, -h, -h), axis=(0, 1, 2))
+        acc += np.roll(w3d_threshold(Vh, sigma, levels, lam_scale), (-h, -h, -h), axis=(0, 1, 2))
     return acc / len(shifts)
 
 
@@ -145,13 +165,13 @@ def tv3d(G: np.ndarray) -> float:
 
 
 def stage1(noisy: np.ndarray, idx: np.ndarray, n_valid: np.ndarray, patch: int, sigma: float,
-           levels: int = 3, shifts=(0, 1)) -> np.ndarray:
+           levels: int = 3, shifts=(0, 1), lam_scale: float = 1.0) -> np.ndarray:
     """phi(Z) for tiling references (stride = N): the filtered volume's groups are aggregated
     at their blocks' positions with weights 1 / TV, first n_valid blocks."""
     H, W = noisy.shape
     N = patch
     V = oracle.gather_volume(noisy, idx, N).astype(np.float64)   # [K, H, W]
-    U = filter_volume(V, sigma, levels, shifts)
+    U = filter_volume(V, sigma, levels, shifts, lam_scale)
     Ry, Rx, K = idx.shape
     num = np.zeros((H, W))
     den = np.zeros((H, W))

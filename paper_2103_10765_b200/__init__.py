@@ -15,6 +15,7 @@ __all__ = [
     "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
     "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
     "last_launch_count", "version", "gather_groups", "gather_volume", "wiener_stage2",
+    "stage1_denoise",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,6 +64,9 @@ def load_library():
         "gbm3d_gather_groups": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp]),
         "gbm3d_gather_volume": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, vp]),
         "gbm3d_wiener_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32]),
+        "gbm3d_stage1_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32, i32, i32]),
+        "gbm3d_stage1_denoise": (i32, [vp, i32, i32, i32, i32, vp, vp, i32, vp, i32, vp, vp,
+                                       ctypes.c_size_t, vp]),
         "gbm3d_wiener_stage2": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp,
                                       vp, ctypes.c_size_t, vp]),
         "gbm3d_last_launch_count": (i32, []),
@@ -319,4 +323,36 @@ def wiener_stage2(noisy, basic, idx, n_valid, patch: int, sigma, out=None, works
         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_handle(noisy.device))
     if st != 0:
         raise GBM3DError(st, "wiener_stage2")
+    return out
+
+
+def stage1_denoise(noisy, idx, n_valid, patch: int, sigma, levels: int = 3, out=None,
+                   workspace=None):
+    """Stage-1 global volume hard thresholding: noisy int16
+    CUDA [(B,) H, W], tables of ``block_match(noisy, patch, patch, ...)`` (tiling references).
+    Returns the float32 estimate [(B,) H, W]."""
+    import torch
+    _check_cuda_int16(noisy, "noisy")
+    _check_cuda_int32(idx, "idx")
+    _check_cuda_int32(n_valid, "n_valid")
+    batched = noisy.dim() == 3
+    B = noisy.shape[0] if batched else 1
+    H, W = noisy.shape[-2], noisy.shape[-1]
+    K = idx.shape[-1]
+    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
+    if sig.numel() == 1:
+        sig = sig.expand(B)
+    sig = sig.contiguous().to(noisy.device)
+    if out is None:
+        out = torch.empty(noisy.shape, dtype=torch.float32, device=noisy.device)
+    need = int(load_library().gbm3d_stage1_workspace_bytes(B, H, W, patch, K))
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=noisy.device)
+    st = load_library().gbm3d_stage1_denoise(
+        ctypes.c_void_p(noisy.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()),
+        ctypes.c_void_p(n_valid.data_ptr()), K, ctypes.c_void_p(sig.data_ptr()), levels,
+        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+        _stream_handle(noisy.device))
+    if st != 0:
+        raise GBM3DError(st, "stage1_denoise")
     return out
