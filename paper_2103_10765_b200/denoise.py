@@ -1,0 +1,52 @@
+"""The whole G-BM3D denoiser composed from the library's kernels (section IV-V).
+
+Every arithmetic step runs in libgbm3d.so: block matching (``block_match``), stage-1 global
+volume hard thresholding (``stage1_denoise``), stage-2 collaborative Wiener filtering
+(``wiener_stage2``).  What this module adds is the paper's schedule around them, with torch used
+only for circular shifts, rounding and averaging of whole images (plumbing):
+
+* stage 1: Y_f = (1/H) sum_h S_-h phi(S_h Z) over the translation trials
+  h = 0, N/4, N/2 of the tiling reference grid (each trial matches its shifted image);
+* stage 2: matching on the basic estimate (rounded to int16), Wiener
+  filtering of the noisy image's groups with the basic estimate's spectra, aggregation.
+
+Parameters default to the paper's except where the library's shapes differ
+(DESIGN.md): stage 1 uses N = 8 tiles with K = 16, stage 2 N = 8 blocks on a stride-3 grid with
+K = 32, both with a search radius of 16 (the paper's window "32").
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+from . import block_match, stage1_denoise, wiener_stage2
+
+
+def stage1(noisy, sigma, patch: int = 8, K: int = 16, radius: int = 16,
+           trials: Optional[Sequence[int]] = None, levels: int = 3):
+    """Basic estimate (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA)."""
+    import torch
+    trials = (0, patch // 4, patch // 2) if trials is None else tuple(trials)
+    dims = (-2, -1)
+    acc = None
+    for h in trials:
+        z = torch.roll(noisy, shifts=(h, h), dims=dims).contiguous() if h else noisy
+        idx, dist, nv = block_match(z, patch, patch, radius, K, None, check=False)
+        y = stage1_denoise(z, idx, nv, patch, sigma, levels)
+        y = torch.roll(y, shifts=(-h, -h), dims=dims) if h else y
+        acc = y if acc is None else acc + y
+    return acc / len(trials)
+
+
+def stage2(noisy, basic, sigma, patch: int = 8, stride: int = 3, K: int = 32, radius: int = 16):
+    """Final estimate from the basic estimate (float32 CUDA, same shape as ``noisy``)."""
+    import torch
+    est = torch.round(basic).clamp_(-32768, 32767).to(torch.int16).contiguous()
+    idx, dist, nv = block_match(est, patch, stride, radius, K, None, check=False)
+    return wiener_stage2(noisy, basic.contiguous(), idx, nv, patch, sigma)
+
+
+def denoise(noisy, sigma, two_stage: bool = True):
+    """G-BM3D1 (stage 1 only) or G-BM3D2 (both stages) of int16 CUDA images [(B,) H, W];
+    H and W must be multiples of 16 (stage-1 tiling and wavelet levels)."""
+    basic = stage1(noisy, sigma)
+    return stage2(noisy, basic, sigma) if two_stage else basic
