@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
             for (int kk = 0; kk < K; ++kk) {
                 const float t2 = tb[kk] * tb[kk];
                 const float dn = t2 + s2;
-                const float wv = dn > 0.f ? t2 / dn : 1.f;
+                const float wv = dn > 0.f ? __fdividef(t2, dn) : 1.f;  // 2 ulp: far below W6
                 n2 = fmaf(wv, wv, n2);
                 tz[kk] *= wv;
             }
