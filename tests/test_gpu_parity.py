@@ -257,3 +257,26 @@ def test_deterministic_repeat():
     b = g.block_match(img, 12, 4, 19, 16, 720000)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+def test_fuzz_wide():
+    """80 random cases per method family: shapes on and off the fast paths (the tensor-core
+    product kernels take P8 s3 r<=21 K<=32; the strip kernel its four shapes; the rest the
+    direct kernel), natural-looking and uniform images, thresholds from 0 to above the int32
+    key range, batched and single calls, all bit-exact against the oracle."""
+    from synth import make_image
+    rng = np.random.default_rng(2024)
+    shapes = [(8, 3), (8, 3), (8, 3), (12, 4), (8, 2), (8, 4), (5, 2), (16, 16), (8, 8), (4, 1)]
+    for case in range(80):
+        P, s = shapes[case % len(shapes)]
+        H = int(rng.integers(P, 120))
+        W = int(rng.integers(P, 120))
+        r = int(rng.integers(0, 33))
+        K = int(rng.integers(1, 65))
+        tau = [None, int(rng.integers(0, 400000)), int(rng.integers(0, 1 << 33))][case % 3]
+        if case % 2:
+            img = make_image(H, W, 6, 2, float(rng.uniform(5, 50)), case)
+        else:
+            img = special_image("uniform", H, W, seed=case, lo=-150, hi=400)
+        _assert_same(_gpu(img, P, s, r, K, tau), oracle.block_match(img, P, s, r, K, tau),
+                     f"wide fuzz {case}: {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
