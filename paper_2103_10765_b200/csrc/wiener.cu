@@ -164,13 +164,21 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = lane % K, gslot = lane / K;
     const int ngroups = ny * nx;
-    for (int g0 = warp * GPW; g0 < ngroups; g0 += (WTHREADS / 32) * GPW) {
+    // the table entries of the warp's next pass are loaded one pass ahead
+    auto fetch = [&](int g0, int& c, int& nv) {
         const int g = g0 + gslot;
         const bool live = g < ngroups;  // uniform per K-lane group
         const int gy = ty0 + (live ? g / nx : 0), gx = tx0 + (live ? g % nx : 0);
         const int64_t ref = ((int64_t)b * Ry + gy) * Rx + gx;
-        const int c = live ? __ldg(idx + ref * K + k) : 0;
-        const int nv = live ? __ldg(nvalid + ref) : 0;
+        c = live ? __ldg(idx + ref * K + k) : 0;
+        nv = live ? __ldg(nvalid + ref) : 0;
+    };
+    int c_next, nv_next;
+    fetch(warp * GPW, c_next, nv_next);
+    for (int g0 = warp * GPW; g0 < ngroups; g0 += (WTHREADS / 32) * GPW) {
+        const bool live = g0 + gslot < ngroups;
+        const int c = c_next, nv = nv_next;
+        fetch(g0 + (WTHREADS / 32) * GPW, c_next, nv_next);
         const int cy = c / W, cx = c - cy * W;
         // 2D DCT of this lane's block, basic estimate (src 0) and noisy image (src 1), into the
         // warp's rows (one copy of the transform code: the kernel is instruction-cache bound)
@@ -214,16 +222,18 @@ __global__ void __launch_bounds__(WTHREADS) wiener_tile_kernel(
             }
             haar_u<K>(tb, false);
             haar_u<K>(tz, false);
-            float n2 = 0.f;
+            float n2p[4] = {0.f, 0.f, 0.f, 0.f};  // four independent accumulation chains
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) {
-                // W = T_B^2 / (T_B^2 + s2) with T_B^2 = D^2 tb^2  ==  tb^2 / (tb^2 + s2 / D^2)
+                // W = T_B^2 / (T_B^2 + s2) with T_B^2 = D^2 tb^2  ==  tb^2 / (tb^2 + s2 / D^2);
+                // 0/0 (sigma = 0 and T_B = 0) gives NaN and fminf(NaN, 1) = 1, the W3 reading
                 const float t2 = tb[kk] * tb[kk];
                 const float dn = fmaf(s2, 1.0f / haar_dsq<K>(kk), t2);
-                const float wv = dn > 0.f ? __fdividef(t2, dn) : 1.f;  // 2 ulp: far below W6
-                n2 = fmaf(wv, wv, n2);
+                const float wv = fminf(__fdividef(t2, dn), 1.f);  // 2 ulp: far below W6
+                n2p[kk & 3] = fmaf(wv, wv, n2p[kk & 3]);
                 tz[kk] *= wv * haar_dsq<K>(kk);
             }
+            const float n2 = (n2p[0] + n2p[1]) + (n2p[2] + n2p[3]);
 #pragma unroll
             for (int q = 0; q < GPW; ++q) n2g[q] += q == qg ? n2 : 0.f;
             haar_u<K>(tz, true);
