@@ -168,7 +168,7 @@ int gbm3d_wiener_stage2(const int16_t* noisy, const float* basic, int B, int H, 
  * (circular shifts of V by h along all three axes), and aggregated with the group weights
  * 1 / TV(U_pq) (anisotropic 3D total variation), pad blocks left out.
  * noisy: device int16 [B][H][W]; sigmas: device float32 [B]; out: device float32 [B][H][W];
- * workspace: gbm3d_stage1_workspace_bytes(B, H, W, patch, K) bytes (4 float volumes + 2 planes).
+ * workspace: gbm3d_stage1_workspace_bytes(B, H, W, patch, K) bytes (3 float volumes + 2 planes).
  * fp32 with atomic accumulation: matches a float64 evaluation within DESIGN.md's tolerance.
  * The translation trials of PAPER.md:203 (match and filter circularly shifted images, shift
  * back, average) are the caller's: each trial is a gbm3d_block_match + gbm3d_stage1_denoise.

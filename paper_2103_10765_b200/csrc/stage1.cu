@@ -28,18 +28,10 @@
 namespace gbm3d {
 namespace {
 
-// bior1.5 analysis lowpass on n = -4..5 (x sqrt2/256), synthesis lowpass = Haar; highpasses by
-// the biorthogonal QMF relations g~[n] = (-1)^n h[1-n], g[n] = (-1)^n h~[1-n].  The constants are
-// the CDF(1,5) integers; the scaling is applied in the kernels.
-__constant__ float kHan[10] = {3.f, -3.f, -22.f, 22.f, 128.f, 128.f, 22.f, -22.f, -3.f, 3.f};
-
-__device__ __forceinline__ float han(int n) {  // n in [-4, 5]
-    return kHan[n + 4] * 0.005524271728019903f;  // sqrt(2) / 256
-}
-__device__ __forceinline__ float gsy(int n) {  // g[n] = (-1)^n h~[1 - n], n in [-4, 5]
-    const float v = han(1 - n);
-    return (n & 1) ? -v : v;
-}
+// bior1.5 (CDF(1,5)): analysis lowpass h~ = (3, -3, -22, 22, 128, 128, 22, -22, -3, 3) sqrt2/256 on
+// n = -4..5, synthesis lowpass = Haar; highpasses by the biorthogonal QMF relations
+// g~[n] = (-1)^n h[1-n], g[n] = (-1)^n h~[1-n].  The passes use them in sum / difference form
+// (ana_step, syn_step) with the constants as instruction immediates.
 constexpr float kR2 = 0.70710678118654752f;
 
 __device__ __forceinline__ int wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
@@ -48,149 +40,375 @@ __device__ __forceinline__ int wrap(int i, int n) { return i < 0 ? i + n : (i >=
 // runtime sizes in the streaming loops.
 constexpr int TPB = 128;
 
-// V[b][k][y][x] = Z_b at the k-th block of the tile containing (y, x), as float; a thread
-// copies one block row (N pixels) of one tile
-__global__ void __launch_bounds__(TPB) s1_volume_kernel(const int16_t* __restrict__ noisy,
-        const int32_t* __restrict__ idx, int K, int H, int W, int N, float* __restrict__ V) {
-    const int Bx = W / N, By = H / N;
-    const int q = blockIdx.x * TPB + threadIdx.x, y = blockIdx.y, s = blockIdx.z;  // s = b K + k
-    if (q >= Bx) return;
+// ---- fused 2D passes: one level of analysis (x then y) or synthesis (y then x) per launch ----
+// A CTA owns a 32 x 32 tile of every subband of one slice.  Analysis stages the 73 x 73 inputs of
+// its outputs (rows and columns 2 i - 4 .. 2 i + 5, periodic in the band) in shared memory, runs
+// the x pass into two shared 73 x 32 planes (a | d) and the y pass from those straight to the
+// four subbands: one read and one write of the band per level instead of two of each.  Synthesis
+// mirrors it: the 68 x 68 coefficients its 64 x 64 outputs need (a[j] and d[j-2 .. j+2] along
+// both axes), y pass into a shared 64 x 68 plane, x pass into a staged 64 x 64 output tile
+// written (or, at level 1, accumulated unshifted into U) row by row.
+constexpr int FT = 32;                 // coefficient tile (per subband)
+constexpr int FIN = 2 * FT + 9;        // 73 analysis inputs per axis
+constexpr int FTHREADS = 256;
+constexpr int SYN_IN = FT + FT + 4;    // 68: a[j0 .. j0+31] then d[j0-2 .. j0+33]
+
+__device__ __forceinline__ int mod_pos(int i, int n) {
+    const int r = i % n;
+    return r < 0 ? r + n : r;
+}
+
+// One analysis step on 5 consecutive input pairs P_m = (x_{2m}, x_{2m+1}), m = i-2 .. i+2, in the
+// sum / difference form of the bior1.5 filters: with S_m = x_{2m} + x_{2m+1}, D_m = x_{2m+1} -
+// x_{2m} the lowpass sum_n h~[n] x_{2i+n} (taps (3, -3, -22, 22, 128, 128, 22, -22, -3, 3) sqrt2/256)
+// is sqrt2/256 (128 S_i + 22 (D_{i-1} - D_{i+1}) + 3 (D_{i+2} - D_{i-2})) and the highpass
+// (x_{2i} - x_{2i+1}) / sqrt2 = -D_i / sqrt2.
+constexpr float kS22 = 22.0f * 0.005524271728019903f, kS3 = 3.0f * 0.005524271728019903f;
+__device__ __forceinline__ void ana_step(const float (&D)[5], float S2, float& a, float& d) {
+    a = fmaf(kS3, D[4] - D[0], fmaf(kS22, D[1] - D[3], kR2 * S2));
+    d = -kR2 * D[2];
+}
+
+// One synthesis step: outputs x[2j], x[2j+1] from a[j] and d[j-2 .. j+2] (D[0..4]):
+// x[m] = h[m & 1] a[m >> 1] + sum_n g[n] d[(m - n) / 2] with g[n] = (-1)^n h~[1 - n] gives
+// x[2j] = a/sqrt2 + P + d_j/sqrt2, x[2j+1] = a/sqrt2 + P - d_j/sqrt2,
+// P = sqrt2/256 (3 (d_{j+2} - d_{j-2}) + 22 (d_{j-1} - d_{j+1})).
+__device__ __forceinline__ void syn_step(const float (&D)[5], float a, float& e, float& f) {
+    const float base = fmaf(kS3, D[4] - D[0], fmaf(kS22, D[1] - D[3], kR2 * a));
+    e = fmaf(kR2, D[2], base);
+    f = fmaf(-kR2, D[2], base);
+}
+
+// src: band [0, h) x [0, w) of slice s at row offset `src_row0` (level 1: the volume V itself,
+// read as S_shift V); LL -> ll_dst (row offset ll_row0), the three detail bands -> det (at their
+// in-place positions).  Slices are H x W with row pitch W.
+// GATHER (level 1): the band is the volume V of matched blocks, read straight from the image:
+// V[k][y][x] = Z[cy + y mod N][cx + x mod N] with (cy, cx) = idx of the tile (y / N, x / N) and
+// slot k, the cycle spin's circular shift applied to (k, y, x) first; `src`
+// is then unused.  Otherwise `src` holds the band (the previous level's LL).
+template <bool GATHER>
+__global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __restrict__ src,
+        int src_row0, const int16_t* __restrict__ img, const int32_t* __restrict__ idx, int N,
+        float* __restrict__ ll_dst, int ll_row0, float* __restrict__ det, int K, int H,
+        int W, int h, int w, int shift) {
+    __shared__ float in[FIN][FIN];            // odd pitch: row-per-lane reads conflict-free
+    __shared__ float xa[FIN][FT + 1], xd[FIN][FT + 1];
+    // per input row / column: offset inside the block (GATHER) or in the band, and the local
+    // tile-block index; the tile's table entries idx[p][q][k] for its <= NBT x NBT blocks
+    constexpr int NBT = (FIN + 3) / 4 + 1;    // blocks per axis for N >= 4
+    __shared__ int rtab[FIN], rl[FIN], ctab[FIN], cl[FIN];
+    __shared__ int rblk[NBT], cblk[NBT];
+    __shared__ int ttab[NBT][NBT];
+    const int hh = h >> 1, wh = w >> 1;
+    const int i0 = blockIdx.y * FT, j0 = blockIdx.x * FT, s = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t plane = (int64_t)H * W;
     const int k = s % K, b = s / K;
-    const int p = y / N, i = y - p * N;
-    const int c = __ldg(idx + (((int64_t)b * By + p) * Bx + q) * K + k);
-    const int cy = c / W, cx = c - cy * W;
-    const int16_t* src = noisy + ((int64_t)b * H + cy + i) * W + cx;
-    float* dst = V + ((int64_t)s * H + y) * W + q * N;
-    for (int j = 0; j < N; ++j) dst[j] = (float)__ldg(src + j);
-}
-
-// analysis along x of the band [0, h) x [0, w) of every slice: out row = [a | d]; a CTA makes
-// TPB outputs of one row from a shared copy of the 2 TPB + 9 inputs it needs (loaded with the
-// periodic wrap -- and, for the cycle spin, the circular shift -- resolved once per input);
-// `shift` > 0 reads the source shifted by `shift` along k, y and x (S_h V)
-__global__ void __launch_bounds__(TPB) s1_ana_x_kernel(const float* __restrict__ src,
-        float* __restrict__ dst, int K, int H, int W, int w, int shift) {
-    __shared__ float xs[2 * TPB + 10];
-    const int half = w >> 1;
-    const int i0 = blockIdx.x * TPB, y = blockIdx.y, s = blockIdx.z;
-    const float* row;
-    if (shift) {
-        const int k = s % K, b = s / K;
-        row = src + ((int64_t)(b * K + wrap(k - shift, K)) * H + wrap(y - shift, H)) * W;
-    } else {
-        row = src + ((int64_t)s * H + y) * W;
-    }
-    const int M = shift ? W : w;
-    for (int j = threadIdx.x; j < 2 * TPB + 10; j += TPB) {
-        const int pos = 2 * i0 - 4 + j;        // band position, in [-4, w + 6)
-        int xi = wrap(min(pos, w + 5), w);
-        xi = shift ? wrap(xi - shift, M) : xi;
-        xs[j] = row[xi];
-    }
-    __syncthreads();
-    const int i = i0 + threadIdx.x;
-    if (i >= half) return;
-    const float* q = xs + 2 * threadIdx.x + 4;  // q[t] = x[2i + t]
-    float a = 0.f;
-#pragma unroll
-    for (int t = -4; t <= 5; ++t) a = fmaf(han(t), q[t], a);
-    const float d = (q[0] - q[1]) * kR2;
-    float* o = dst + ((int64_t)s * H + y) * W;
-    o[i] = a;
-    o[half + i] = d;
-}
-
-// analysis along y: a thread walks down one column of the band, RY outputs per CTA row, with the
-// 10 input rows of the current output in a sliding register window (each input read once)
-constexpr int RY = 16;
-__global__ void __launch_bounds__(TPB) s1_ana_y_kernel(const float* __restrict__ src,
-        float* __restrict__ dst, int H, int W, int h, int w) {
-    const int half = h >> 1;
-    const int x = blockIdx.x * TPB + threadIdx.x, s = blockIdx.z;
-    const int i0 = blockIdx.y * RY;
-    if (x >= w) return;
-    const float* col = src + (int64_t)s * H * W + x;
-    float* o = dst + (int64_t)s * H * W + x;
-    float win[10];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) win[t] = col[(int64_t)wrap(2 * i0 - 4 + t, h) * W];
-    for (int i = i0; i < min(i0 + RY, half); ++i) {
-        win[8] = col[(int64_t)wrap(2 * i + 4, h) * W];
-        win[9] = col[(int64_t)wrap(2 * i + 5, h) * W];
-        float a = 0.f;
-#pragma unroll
-        for (int t = 0; t < 10; ++t) a = fmaf(han(t - 4), win[t], a);
-        o[(int64_t)i * W] = a;
-        o[(int64_t)(half + i) * W] = (win[4] - win[5]) * kR2;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) win[t] = win[t + 2];
-    }
-}
-
-// synthesis along y: x[m] = h[m & 1] a[m >> 1] + sum_{n = m (mod 2)} g[n] d[(m - n) / 2];
-// for an output pair (2j, 2j+1) the details d[j-2 .. j+2] and a[j] suffice: sliding window
-__global__ void __launch_bounds__(TPB) s1_syn_y_kernel(const float* __restrict__ src,
-        float* __restrict__ dst, int H, int W, int h, int w) {
-    const int half = h >> 1;
-    const int x = blockIdx.x * TPB + threadIdx.x, s = blockIdx.z;
-    const int j0 = blockIdx.y * RY;
-    if (x >= w) return;
-    const float* col = src + (int64_t)s * H * W + x;
-    float* o = dst + (int64_t)s * H * W + x;
-    float dw[5];  // d[j - 2 .. j + 2]
-#pragma unroll
-    for (int t = 0; t < 4; ++t) dw[t] = col[(int64_t)(half + wrap(j0 - 2 + t, half)) * W];
-    for (int j = j0; j < min(j0 + RY, half); ++j) {
-        dw[4] = col[(int64_t)(half + wrap(j + 2, half)) * W];
-        const float aj = col[(int64_t)j * W];
-        // m = 2j   : n even, (m - n)/2 = j - n/2, n in {-4,-2,0,2,4} -> d[j+2], d[j+1], d[j], d[j-1], d[j-2]
-        // m = 2j+1 : n odd,  (m - n)/2 = j - (n-1)/2, n in {-3,-1,1,3,5} -> d[j+2] .. d[j-2]
-        float e = kR2 * aj, f = kR2 * aj;
-#pragma unroll
-        for (int u = 0; u < 5; ++u) {
-            e = fmaf(gsy(2 * (2 - u)), dw[u], e);       // n = 4 - 2u pairs with d[j - 2 + u]
-            f = fmaf(gsy(2 * (2 - u) + 1), dw[u], f);   // n = 5 - 2u
+    const int ks = GATHER ? mod_pos(k - shift, K) : k;
+    const float* const slice = src + (int64_t)s * plane + (int64_t)src_row0 * W;
+    const int16_t* const zimg = img + (int64_t)b * plane;
+    const bool table = GATHER && N >= 4;
+    if (tid < FIN) {
+        const int y = mod_pos(mod_pos(2 * i0 - 4 + tid, h) - shift, GATHER ? H : h);
+        if (GATHER) {
+            const int pb = y / N;
+            rtab[tid] = (y - pb * N) * W;                                  // row within the block
+            // H is a multiple of N, so the block changes every N rows, across the wrap too
+            const int y0 = mod_pos(2 * i0 - 4 - shift, H);
+            const int lr = (tid + y0 % N) / N;
+            rl[tid] = lr;
+            const int blk = ((b * (H / N) + pb) * (W / N)) * K + ks;      // table row of the tile
+            if (table) {
+                if (tid == 0 || (y - pb * N) == 0) rblk[lr] = blk;
+            } else {
+                rl[tid] = blk;                                             // N < 4: direct lookups
+            }
+        } else {
+            rtab[tid] = y * W;
         }
-        o[(int64_t)(2 * j) * W] = e;
-        o[(int64_t)(2 * j + 1) * W] = f;
+    } else if (tid >= 128 && tid < 128 + FIN) {
+        const int c = tid - 128;
+        const int x = mod_pos(mod_pos(2 * j0 - 4 + c, w) - shift, GATHER ? W : w);
+        if (GATHER) {
+            const int qb = x / N;
+            ctab[c] = x - qb * N;
+            const int x0 = mod_pos(2 * j0 - 4 - shift, W);
+            const int lc = (c + x0 % N) / N;
+            cl[c] = lc;
+            if (table) {
+                if (c == 0 || (x - qb * N) == 0) cblk[lc] = qb * K;
+            } else {
+                cl[c] = qb * K;
+            }
+        } else {
+            ctab[c] = x;
+        }
+    }
+    __syncthreads();
+    if (table) {
+        const int nb = (FIN - 1 + N - 1) / N + 1;   // local blocks per axis
+        for (int e = tid; e < nb * nb; e += FTHREADS) {
+            const int r = e / nb, c = e - r * nb;
+            ttab[r][c] = __ldg(idx + rblk[r] + cblk[c]);
+        }
+        __syncthreads();
+    }
+    {
+        // rows warp, warp + 8, ..; lanes on columns lane + 32 m: every load of the thread in
+        // flight before its first shared store
+        constexpr int RPW = (FIN + 7) / 8;
+        int cofs[3], cq[3];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) dw[t] = dw[t + 1];
+        for (int m = 0; m < 3; ++m) {
+            const int c = min(lane + 32 * m, FIN - 1);
+            cofs[m] = ctab[c];
+            cq[m] = GATHER ? cl[c] : 0;
+        }
+        float v[RPW][3];
+        if (GATHER) {
+            int cpos[RPW][3];
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = min(warp + 8 * q, FIN - 1);
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    cpos[q][m] = table ? ttab[rl[r]][cq[m]] : __ldg(idx + rl[r] + cq[m]);
+            }
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = warp + 8 * q;
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    if (r < FIN && lane + 32 * m < FIN)
+                        v[q][m] = (float)__ldg(zimg + cpos[q][m] + rtab[r] + cofs[m]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = warp + 8 * q;
+                if (r < FIN) {
+                    const float* rp = slice + rtab[r];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m)
+                        if (lane + 32 * m < FIN) v[q][m] = __ldg(rp + cofs[m]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const int r = warp + 8 * q;
+            if (r < FIN) {
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    if (lane + 32 * m < FIN) in[r][lane + 32 * m] = v[q][m];
+            }
+        }
+    }
+    __syncthreads();
+    // x pass: item = (row r, segment of 11 | 11 | 10 outputs), a sliding window of 5 pairs
+    if (tid < 3 * FIN) {
+        const int seg = tid / FIN, r = tid - seg * FIN;
+        const int jb = seg * 11;
+        float D[5], S2, S3;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const float x0 = in[r][2 * (jb + m)], x1 = in[r][2 * (jb + m) + 1];
+            D[m] = x1 - x0;
+            if (m == 2) S2 = x0 + x1;
+            if (m == 3) S3 = x0 + x1;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 11; ++jj) {
+            const int j = jb + jj;
+            if (j >= FT) break;
+            const float x0 = in[r][2 * j + 8], x1 = in[r][2 * j + 9];
+            D[4] = x1 - x0;
+            const float S4 = x0 + x1;
+            float a, d;
+            ana_step(D, S2, a, d);
+            xa[r][j] = a;
+            xd[r][j] = d;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) D[t] = D[t + 1];
+            S2 = S3;
+            S3 = S4;
+        }
+    }
+    __syncthreads();
+    // y pass: item = (column c of [a | d], segment of 8 outputs); a warp = 32 consecutive columns
+    {
+        const int c = tid & 63, seg = tid >> 6;
+        const int j = c & 31;
+        const bool dcol = c >= 32;
+        const float(*xs)[FT + 1] = dcol ? xd : xa;
+        const int ib = seg * 8;
+        float D[5], S2, S3;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const float x0 = xs[2 * (ib + m)][j], x1 = xs[2 * (ib + m) + 1][j];
+            D[m] = x1 - x0;
+            if (m == 2) S2 = x0 + x1;
+            if (m == 3) S3 = x0 + x1;
+        }
+        float* const lo_base = dcol ? det + (int64_t)s * plane : ll_dst + (int64_t)s * plane + (int64_t)ll_row0 * W;
+        float* const hi_base = det + (int64_t)s * plane;
+        const int xo = dcol ? wh + j0 + j : j0 + j;
+        const bool colok = j0 + j < wh;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = ib + u;
+            const float x0 = xs[2 * i + 8][j], x1 = xs[2 * i + 9][j];
+            D[4] = x1 - x0;
+            const float S4 = x0 + x1;
+            float a, d;
+            ana_step(D, S2, a, d);
+            if (colok && i0 + i < hh) {
+                lo_base[(int64_t)(i0 + i) * W + xo] = a;
+                hi_base[(int64_t)(hh + i0 + i) * W + xo] = d;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) D[t] = D[t + 1];
+            S2 = S3;
+            S3 = S4;
+        }
     }
 }
 
-// synthesis along x of one row segment: outputs m in [m0, m0 + 2 TPB) from shared copies of
-// a[m0/2 .. m0/2 + TPB) and d[m0/2 - 2 .. m0/2 + TPB + 2); for the last level (accumulate != 0)
-// U[S_-h] += scale * result
-__global__ void __launch_bounds__(TPB) s1_syn_x_kernel(const float* __restrict__ src,
-        float* __restrict__ dst, int K, int H, int W, int w, int shift, float scale, int accumulate) {
-    __shared__ float as_[TPB], ds_[TPB + 4];
-    const int half = w >> 1;
-    const int j0 = blockIdx.x * TPB, y = blockIdx.y, s = blockIdx.z;
-    const float* row = src + ((int64_t)s * H + y) * W;
-    if (j0 + threadIdx.x < half) as_[threadIdx.x] = row[j0 + threadIdx.x];
-    for (int t = threadIdx.x; t < TPB + 4; t += TPB) ds_[t] = row[half + wrap(j0 - 2 + t, half)];
-    __syncthreads();
-    const int j = j0 + threadIdx.x;
-    if (j >= half) return;
-    const float aj = as_[threadIdx.x];
-    float e = kR2 * aj, f = kR2 * aj;
-#pragma unroll
-    for (int u = 0; u < 5; ++u) {
-        const float dv = ds_[threadIdx.x + u];  // d[j - 2 + u]
-        e = fmaf(gsy(2 * (2 - u)), dv, e);
-        f = fmaf(gsy(2 * (2 - u) + 1), dv, f);
+// synthesis of one level: LL (ll_src at row offset ll_row0) and the detail bands (det) of the
+// band [0, h) x [0, w) -> the band's reconstruction: written to dst at row offset dst_row0, or
+// (accumulate) added as scale x S_-shift into U.
+__global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __restrict__ ll_src,
+        int ll_row0, const float* __restrict__ det, float* __restrict__ dst, int dst_row0, int K,
+        int H, int W, int h, int w, int shift, float scale, int accumulate) {
+    __shared__ float cf[SYN_IN][SYN_IN + 1];       // [y: a rows | d rows][x: a cols | d cols]
+    __shared__ float ty[2 * FT][SYN_IN + 1];       // after the y pass: 64 rows x [a | d] cols
+    __shared__ int rtab[SYN_IN], ctab[SYN_IN];
+    const int hh = h >> 1, wh = w >> 1;
+    const int i0 = blockIdx.y * FT, j0 = blockIdx.x * FT, s = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t plane = (int64_t)H * W;
+    // coefficient rows/columns: a at i0 + t (t < 32; beyond the band: unused), d at hh + (i0 - 2
+    // + t - 32 mod hh)
+    if (tid < SYN_IN)
+        rtab[tid] = tid < FT ? min(i0 + tid, hh - 1) : hh + mod_pos(i0 - 2 + tid - FT, hh);
+    else if (tid < 2 * SYN_IN) {
+        const int t = tid - SYN_IN;
+        ctab[t] = t < FT ? min(j0 + t, wh - 1) : wh + mod_pos(j0 - 2 + t - FT, wh);
     }
-    const int m = 2 * j;
-    if (!accumulate) {
-        float* o = dst + ((int64_t)s * H + y) * W;
-        o[m] = e;
-        o[m + 1] = f;
+    __syncthreads();
+    const float* const llp = ll_src + (int64_t)s * plane + (int64_t)ll_row0 * W;
+    const float* const dp = det + (int64_t)s * plane;
+    {
+        // rows warp, warp + 8, ..; lanes on columns lane + 32 m: loads first, then stores
+        constexpr int RPW = (SYN_IN + 7) / 8;
+        int cofs[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) cofs[m] = ctab[min(lane + 32 * m, SYN_IN - 1)];
+        float v[RPW][3];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const int r = warp + 8 * q;
+            if (r < SYN_IN) {
+                const int64_t ro = (int64_t)rtab[r] * W;
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    const int c = lane + 32 * m;
+                    if (c < SYN_IN) v[q][m] = __ldg(((r < FT && c < FT) ? llp : dp) + ro + cofs[m]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const int r = warp + 8 * q;
+            if (r < SYN_IN) {
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    if (lane + 32 * m < SYN_IN) cf[r][lane + 32 * m] = v[q][m];
+            }
+        }
+    }
+    __syncthreads();
+    // y pass: item = (column c, segment of 11 | 11 | 10 output pairs); x[2j] = r2 a[j] +
+    // sum_u g[4 - 2u] d[j - 2 + u], x[2j+1] = r2 a[j] + sum_u g[5 - 2u] d[j - 2 + u]
+    if (tid < 3 * SYN_IN) {
+        const int seg = tid / SYN_IN, c = tid - seg * SYN_IN;
+        const int jb = seg * 11;
+        float dw[5];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dw[t] = cf[FT + jb + t][c];
+#pragma unroll
+        for (int jj = 0; jj < 11; ++jj) {
+            const int j = jb + jj;
+            if (j >= FT) break;
+            dw[4] = cf[FT + j + 4][c];
+            const float aj = cf[j][c];
+            float e, f;
+            syn_step(dw, aj, e, f);
+            ty[2 * j][c] = e;
+            ty[2 * j + 1][c] = f;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dw[t] = dw[t + 1];
+        }
+    }
+    __syncthreads();
+    // x pass: item = (row m, segment of 8 output pairs); the 64 x 64 result overwrites cf
+    float(*const out)[SYN_IN + 1] = cf;
+    {
+        const int m = tid & 63, seg = tid >> 6;
+        const int jb = seg * 8;
+        float dw[5];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dw[t] = ty[m][FT + jb + t];
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) {
+            const int j = jb + u8;
+            dw[4] = ty[m][FT + j + 4];
+            const float aj = ty[m][j];
+            float e, f;
+            syn_step(dw, aj, e, f);
+            out[m][2 * j] = e;
+            out[m][2 * j + 1] = f;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dw[t] = dw[t + 1];
+        }
+    }
+    __syncthreads();
+    const int y0 = 2 * i0, x0 = 2 * j0;
+    const int c = tid & 63, x = x0 + c;
+    if (x >= w) return;
+    constexpr int RPT = 2 * FT / (FTHREADS / 64);   // 16 rows per thread
+    if (accumulate == 0) {
+        float* const o = dst + (int64_t)s * plane + (int64_t)dst_row0 * W + x;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int r = (tid >> 6) + q * (FTHREADS / 64);
+            if (y0 + r < h) o[(int64_t)(y0 + r) * W] = out[r][c];
+        }
     } else {
-        // (S_-h R)[k][y][x] = R[k + h][y + h][x + h]: this R element lands at (k-h, y-h, x-h)
+        // (S_-h R)[k][y][x] = R[k + h][y + h][x + h]: this element lands at (k-h, y-h, x-h)
+        // (level 1: the band is the whole slice, h = H, w = W, 0 <= shift < H, W, K).  The first
+        // spin stores (accumulate = 1: U needs no clearing), later ones add (accumulate = 2),
+        // every load of the thread in flight before its first store.
         const int k = s % K, b = s / K;
-        float* o = dst + ((int64_t)(b * K + wrap(k - shift, K)) * H + wrap(y - shift, H)) * W;
-        o[wrap(m - shift, W)] += scale * e;
-        o[wrap(m + 1 - shift, W)] += scale * f;
+        const int kk = k >= shift ? k - shift : k - shift + K;
+        const int xs = x >= shift ? x - shift : x - shift + W;
+        float* const o = dst + (int64_t)(b * K + kk) * plane + xs;
+        int64_t ofs[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int y = y0 + (tid >> 6) + q * (FTHREADS / 64);
+            const int ys = y >= shift ? y - shift : y - shift + H;
+            ofs[q] = (int64_t)ys * W;
+        }
+        float old[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+            old[q] = (accumulate == 2 && y0 + (tid >> 6) + q * (FTHREADS / 64) < h) ? o[ofs[q]] : 0.f;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int r = (tid >> 6) + q * (FTHREADS / 64);
+            if (y0 + r < h) o[ofs[q]] = fmaf(scale, out[r][c], old[q]);
+        }
     }
 }
 
@@ -245,53 +463,84 @@ __global__ void __launch_bounds__(TPB) s1_z_kernel(float* __restrict__ C, int H,
     for (int k = 0; k < K; ++k) base[(int64_t)k * plane] = v[k];
 }
 
-// TV of every group U_pq (K x N x N) -> weight 1 / TV (1 when TV = 0); warp per group
-__global__ void s1_tv_kernel(const float* __restrict__ U, int B, int K, int H, int W, int N,
-                             float* __restrict__ wout) {
-    const int Bx = W / N, By = H / N;
-    const int64_t ngroups = (int64_t)B * By * Bx;
-    const int lane = threadIdx.x & 31;
-    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups;
-         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t b = g / (By * Bx);
-        const int pq = (int)(g - b * By * Bx), p = pq / Bx, q = pq - p * Bx;
-        const float* base = U + b * K * (int64_t)H * W + (int64_t)(p * N) * W + q * N;
-        float tv = 0.f;
-        for (int e = lane; e < K * N * N; e += 32) {
-            const int k = e / (N * N), r = e - k * N * N, i = r / N, j = r - i * N;
-            const float u = base[(int64_t)k * H * W + (int64_t)i * W + j];
-            if (k + 1 < K) tv += fabsf(base[(int64_t)(k + 1) * H * W + (int64_t)i * W + j] - u);
-            if (i + 1 < N) tv += fabsf(base[(int64_t)k * H * W + (int64_t)(i + 1) * W + j] - u);
-            if (j + 1 < N) tv += fabsf(base[(int64_t)k * H * W + (int64_t)i * W + j + 1] - u);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
-        if (lane == 0) wout[g] = tv > 0.f ? 1.f / tv : 1.f;
+// TV weight and aggregation of one group per CTA (K N threads): the group's K x N x N values are
+// staged in shared memory in (k, i, j) order (16-byte loads, consecutive threads on consecutive
+// elements: conflict-free), TV = sum of |forward differences| along x, y and z (reading S4) with
+// every thread on elements e, e + nt, ..; w = 1 / TV (1 when TV = 0) by a block reduction; then
+// the first n_valid blocks add w U_pq[k] at their positions (fp32 reductions, consecutive
+// threads on consecutive pixels of a block row) and their weight once at their top-left pixel
+// of the weight map.
+__device__ __forceinline__ void s1_split(int e, int N, int NN, bool p2, int lg, int& k, int& i, int& j) {
+    if (p2) {
+        k = e >> (2 * lg);
+        const int r = e & (NN - 1);
+        i = r >> lg;
+        j = r & (N - 1);
+    } else {
+        k = e / NN;
+        const int r = e - k * NN;
+        i = r / N;
+        j = r - i * N;
     }
 }
 
-// aggregation: block k < n_valid of group (p, q) adds w U_pq[k] at its position (a thread per
-// block row: N reductions); the block's weight goes once to its top-left pixel of the weight
-// map (the divide takes N x N box sums)
-__global__ void __launch_bounds__(512) s1_aggregate_kernel(const float* __restrict__ U,
-        const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid,
-        const float* __restrict__ wg, int K, int H, int W, int N, float* __restrict__ num,
-        float* __restrict__ wmap) {
+__global__ void __launch_bounds__(512) s1_tv_aggregate_kernel(const float* __restrict__ U,
+        const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid, int K, int H, int W,
+        int N, float* __restrict__ num, float* __restrict__ wmap) {
+    extern __shared__ float gsm[];              // [K][N][N], 32 partial sums, K positions
     const int Bx = W / N, By = H / N;
-    const int t = threadIdx.x;                     // (k, i) of the group: blockDim = K N
-    const int g = blockIdx.x, b = blockIdx.y;      // group within image b
-    const int k = t / N, i = t - k * N;
-    const int64_t gi = (int64_t)b * By * Bx + g;
-    if (k >= __ldg(nvalid + gi)) return;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int g = blockIdx.x, b = blockIdx.y;
     const int p = g / Bx, q = g - p * Bx;
-    const int c = __ldg(idx + gi * K + k);
-    const int cy = c / W, cx = c - cy * W;
-    const float w = wg[gi];
+    const int64_t gi = (int64_t)b * By * Bx + g;
     const int64_t plane = (int64_t)H * W;
-    const float* u = U + ((int64_t)b * K + k) * plane + (int64_t)(p * N + i) * W + q * N;
-    float* o = num + b * plane + (int64_t)(cy + i) * W + cx;
-    for (int j = 0; j < N; ++j) atomicAdd(o + j, w * u[j]);
-    if (i == 0) atomicAdd(wmap + b * plane + (int64_t)cy * W + cx, w);
+    const int NN = N * N, KNN = K * NN;
+    const bool p2 = (N & (N - 1)) == 0;
+    const int lg = __ffs(N) - 1;
+    const float* const gbase = U + (int64_t)b * K * plane + (int64_t)(p * N) * W + q * N;
+    int* const pos = reinterpret_cast<int*>(gsm + KNN + 32);     // K block positions
+    if (t < K) pos[t] = __ldg(idx + gi * K + t);
+    if ((N & 3) == 0) {
+        for (int e4 = t; e4 < KNN / 4; e4 += nt) {
+            int k, i, j;
+            s1_split(4 * e4, N, NN, p2, lg, k, i, j);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(gbase + (int64_t)k * plane + (int64_t)i * W + j));
+            *reinterpret_cast<float4*>(gsm + 4 * e4) = v;
+        }
+    } else {
+        for (int e = t; e < KNN; e += nt) {
+            int k, i, j;
+            s1_split(e, N, NN, p2, lg, k, i, j);
+            gsm[e] = __ldg(gbase + (int64_t)k * plane + (int64_t)i * W + j);
+        }
+    }
+    __syncthreads();
+    float tv = 0.f;
+    for (int e = t; e < KNN; e += nt) {
+        int k, i, j;
+        s1_split(e, N, NN, p2, lg, k, i, j);
+        const float u = gsm[e];
+        if (j + 1 < N) tv += fabsf(gsm[e + 1] - u);
+        if (i + 1 < N) tv += fabsf(gsm[e + N] - u);
+        if (k + 1 < K) tv += fabsf(gsm[e + NN] - u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
+    float* const part = gsm + KNN;
+    if ((t & 31) == 0) part[t >> 5] = tv;
+    __syncthreads();
+    float tot = 0.f;
+    for (int wi = 0; wi < (nt + 31) / 32; ++wi) tot += part[wi];
+    const float w = tot > 0.f ? 1.f / tot : 1.f;
+    const int nv = __ldg(nvalid + gi);
+    float* const nb = num + b * plane;
+    for (int e = t; e < nv * NN; e += nt) {
+        int kb, ii, jj;
+        s1_split(e, N, NN, p2, lg, kb, ii, jj);
+        const int c = pos[kb];                              // cy W + cx
+        atomicAdd(nb + (int64_t)c + (int64_t)ii * W + jj, w * gsm[e]);
+        if (ii == 0 && jj == 0) atomicAdd(wmap + b * plane + c, w);
+    }
 }
 
 // out = num / (N x N box sums of the weight map over [y-N+1, y] x [x-N+1, x]): 32 x 32 output
@@ -341,8 +590,7 @@ using namespace gbm3d;
 extern "C" size_t gbm3d_stage1_workspace_bytes(int B, int H, int W, int patch, int K) {
     if (B < 1 || H < 1 || W < 1 || patch < 1 || K < 1) return 0;
     const size_t vol = (size_t)B * K * H * W;
-    const size_t groups = (size_t)B * (H / patch) * (W / patch);
-    return (4 * vol + 2 * (size_t)B * H * W + groups) * sizeof(float);
+    return (3 * vol + 2 * (size_t)B * H * W) * sizeof(float);
 }
 
 extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch,
@@ -357,29 +605,34 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
     if ((K & (K - 1)) != 0 || K > 32 || patch > 16 || levels > 5) return GBM3D_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t vol = (int64_t)B * K * H * W, plane = (int64_t)B * H * W;
-    float* const V = (float*)workspace;   // the volume (kept for both cycle spins)
-    float* const C = V + vol;             // coefficients
+    float* const C = (float*)workspace;   // coefficients
     float* const Tm = C + vol;            // separable-pass scratch
     float* const U = Tm + vol;            // filtered volume (mean of the spins)
     float* const num = U + vol;
     float* const wmap = num + plane;
-    float* const wg = wmap + plane;
     int lz = 0;  // Haar levels along z: min(L, log2 K) (reading S1)
     while ((1 << (lz + 1)) <= K && lz < levels) ++lz;
     const int BK = B * K;
-    if (cudaMemsetAsync(U, 0, (size_t)(vol + 2 * plane) * sizeof(float), s) != cudaSuccess)
+    // U is stored by the first spin's last synthesis pass; the aggregation planes are cleared
+    if (cudaMemsetAsync(num, 0, (size_t)(2 * plane) * sizeof(float), s) != cudaSuccess)
         return GBM3D_ERR_CUDA;
     const unsigned gx = (unsigned)((W + TPB - 1) / TPB);
-    s1_volume_kernel<<<dim3((unsigned)((W / patch + TPB - 1) / TPB), H, BK), TPB, 0, s>>>(
-        noisy, idx, K, H, W, patch, V);
     const int spins = 2;
     for (int sh = 0; sh < spins; ++sh) {
+        // analysis: LL_l goes to the scratch volume at alternating row offsets (odd levels at
+        // row 0, even ones at row H/2: never the rows the same launch reads), the last level's
+        // to C's corner; the details to C at their in-place positions
         for (int l = 1; l <= levels; ++l) {
             const int h = H >> (l - 1), w = W >> (l - 1);
-            s1_ana_x_kernel<<<dim3((unsigned)((w / 2 + TPB - 1) / TPB), h, BK), TPB, 0, s>>>(
-                l == 1 ? V : C, Tm, K, H, W, w, l == 1 ? sh : 0);
-            s1_ana_y_kernel<<<dim3((unsigned)((w + TPB - 1) / TPB), (unsigned)((h / 2 + RY - 1) / RY), BK),
-                              TPB, 0, s>>>(Tm, C, H, W, h, w);
+            const dim3 fg((unsigned)((w / 2 + FT - 1) / FT), (unsigned)((h / 2 + FT - 1) / FT), BK);
+            float* lld = l == levels ? C : Tm;
+            const int ll_row0 = l == levels ? 0 : (l & 1 ? 0 : H / 2);
+            if (l == 1)
+                s1_ana_xy_kernel<true><<<fg, FTHREADS, 0, s>>>(nullptr, 0, noisy, idx, patch, lld, ll_row0,
+                                                               C, K, H, W, h, w, sh);
+            else
+                s1_ana_xy_kernel<false><<<fg, FTHREADS, 0, s>>>(Tm, (l - 1) & 1 ? 0 : H / 2, nullptr, nullptr,
+                                                                patch, lld, ll_row0, C, K, H, W, h, w, 0);
         }
         const dim3 zg(gx, H, B);
         switch (K) {
@@ -390,17 +643,25 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
             case 16: s1_z_kernel<16><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
             default: s1_z_kernel<32><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
         }
+        // synthesis: LL_l from C's corner (l = L) or the scratch offset of level l, LL_(l-1) to
+        // the scratch offset of level l - 1, level 1 accumulated unshifted into U
         for (int l = levels; l >= 1; --l) {
             const int h = H >> (l - 1), w = W >> (l - 1);
-            s1_syn_y_kernel<<<dim3((unsigned)((w + TPB - 1) / TPB), (unsigned)((h / 2 + RY - 1) / RY), BK),
-                              TPB, 0, s>>>(C, Tm, H, W, h, w);
-            s1_syn_x_kernel<<<dim3((unsigned)((w / 2 + TPB - 1) / TPB), h, BK), TPB, 0, s>>>(
-                Tm, l == 1 ? U : C, K, H, W, w, sh, 1.0f / spins, l == 1);
+            const dim3 fg((unsigned)((w / 2 + FT - 1) / FT), (unsigned)((h / 2 + FT - 1) / FT), BK);
+            const float* lls = l == levels ? C : Tm;
+            const int ll_row0 = l == levels ? 0 : (l & 1 ? 0 : H / 2);
+            float* dst = l == 1 ? U : Tm;
+            const int dst_row0 = l == 1 ? 0 : ((l - 1) & 1 ? 0 : H / 2);
+            s1_syn_xy_kernel<<<fg, FTHREADS, 0, s>>>(lls, ll_row0, C, dst, dst_row0, K, H, W, h, w, sh,
+                                                     1.0f / spins, l == 1 ? (sh == 0 ? 1 : 2) : 0);
         }
     }
-    s1_tv_kernel<<<grid1((int64_t)B * (H / patch) * (W / patch) * 32), 256, 0, s>>>(U, B, K, H, W, patch, wg);
-    s1_aggregate_kernel<<<dim3((unsigned)((H / patch) * (W / patch)), B), K * patch, 0, s>>>(
-        U, idx, n_valid, wg, K, H, W, patch, num, wmap);
+    {
+        const int nt = K * patch;
+        const size_t smem = ((size_t)K * patch * patch + 32 + K) * sizeof(float);
+        s1_tv_aggregate_kernel<<<dim3((unsigned)((H / patch) * (W / patch)), B), nt, smem, s>>>(
+            U, idx, n_valid, K, H, W, patch, num, wmap);
+    }
     s1_divide_kernel<<<dim3((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), B), 256, 0, s>>>(
         num, wmap, out, H, W, patch);
     return cudaGetLastError() == cudaSuccess ? GBM3D_OK : GBM3D_ERR_CUDA;

@@ -59,6 +59,22 @@ def test_stage1_parity(H, W, N, K, r, sigma, seed):
     assert np.mean((got - clean) ** 2) < 0.6 * np.mean((noisy.astype(np.float64) - clean) ** 2)
 
 
+@pytest.mark.parametrize("H,W,sigma,seed", [(256, 256, 25.0, 5), (320, 192, 30.0, 6)])
+def test_stage1_parity_multi_tile(H, W, sigma, seed):
+    """Sizes spanning several 32 x 32 coefficient tiles per level (and ragged ones: 320 x 192
+    gives level-3 bands of 40 x 24).  With ~10^6 thresholded coefficients some sit within fp32
+    rounding of lambda, so a few keep/zero decisions may differ from the float64 oracle: nearly
+    every pixel must agree to 1e-2 and the mean difference stay far below one grey level."""
+    N, K, r = 8, 16, 16
+    noisy, clean, sig = make_image(H, W, 10, 4, sigma, seed, return_clean=True)
+    idx, dist, nv = oracle.block_match(noisy, N, N, r, K, None)
+    exp = stage1.stage1(noisy, idx, nv, N, sig)
+    got = _run(noisy, idx, nv, N, sig)
+    diff = np.abs(got - exp)
+    assert np.mean(diff > 1e-2) < 0.02, np.mean(diff > 1e-2)
+    assert diff.mean() < 2e-2, diff.mean()
+
+
 def test_stage1_batched_and_errors():
     g = _g()
     imgs, sigs, tabs = [], [], []

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-for v in w_v4 w_v10 w_v11 w_v4 w_v10 w_v11; do echo $v; GBM3D_LIB=variants/$v.so python tools/dev/time_wiener.py c3; done
-GBM3D_LIB=variants/w_v11.so timeout 900 python -m pytest tests/test_gpu_wiener.py tests/test_gpu_denoise.py -q -x 2>&1 | tail -2
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:s1_(ana_xy|syn_xy)" -c 6 -o gpurun_out/s1_v5 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
