@@ -333,9 +333,10 @@ FP32_FMA_LANES_PER_SM = 64  # FFMA (3-register form): 16 lanes/clk/SMSP (B300_MI
 
 
 def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
-    """stage-2 collaborative Wiener filtering + aggregation of every group of this
-    step's table, the noise-free synthetic image standing in for the basic estimate (DESIGN.md
-    W-readings).  Roofline: fp32 FMA pipe; algorithmic flops per block = three separable 8x8 DCTs
+    """stage-2 collaborative Wiener filtering + aggregation of every group, the
+    noise-free synthetic image standing in for the basic estimate (DESIGN.md W-readings) and the
+    groups matched on it (the step's configuration).  Roofline: fp32 FMA pipe; algorithmic
+    flops per block = three separable 8x8 DCTs
     (2 x 512 FMA each) + three Haar cascades (64 x log2 K butterflies of 2 flops) + shrinkage."""
     from synth import make_image
     if call.patch != 8 or call.K & (call.K - 1):
@@ -346,8 +347,13 @@ def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
              for sd in seeds]
     basic = torch.from_numpy(np.stack([c[1] for c in clean]).astype(np.float32)).to(img.device)
     sig = [c[2] for c in clean]
+    # stage 2 groups the blocks by matching on the basic estimate: the
+    # step's tables come from the noisy image, so match once more on the stand-in (untimed)
+    est = torch.from_numpy(np.stack([c[1] for c in clean]).astype(np.int16)).to(img.device)
     if B == 1:
         basic = basic[0].contiguous()
+        est = est[0].contiguous()
+    outs = g.block_match(est, call.patch, call.stride, call.radius, call.K, call.tau, check=False)
     out = torch.empty(basic.shape, dtype=torch.float32, device=img.device)
     ws = torch.empty(g.load_library().gbm3d_wiener_workspace_bytes(B, cfg.H, cfg.W),
                      dtype=torch.uint8, device=img.device)
@@ -379,9 +385,8 @@ def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
 def run_stage1(args, cfg, call, torch, g, img, flush_buf):
     """stage-1 global volume hard thresholding of the workload's image(s) with
     tiling references (stride = patch = 8, K = 16, the paper's K), matching included in the
-    tables but not in the timing.  HBM roofline: ~28 streaming passes over the K x H x W fp32
-    volume (per spin and level: analysis x/y, z pass, synthesis y/x; plus build, TV,
-    aggregation), counted in DESIGN.md."""
+    tables but not in the timing.  HBM roofline: the fp32 volume traffic of the fused schedule
+    (DESIGN.md 7.7), about 14.5 reads/writes of the K x H x W fp32 volume per call."""
     N, K, levels = 8, 16, 3
     if cfg.H % 16 or cfg.W % 16:
         return None
@@ -397,10 +402,13 @@ def run_stage1(args, cfg, call, torch, g, img, flush_buf):
     times = measure_device(step, args.steps, args.warmup, flush_buf.zero_, torch, soak_s=0.2)
     ms = statistics.mean(times)
     vol = cfg.B * K * cfg.H * cfg.W * 4
-    # per spin: analysis and synthesis each read + write the level-l band twice (x and y
-    # passes: 4 vol / 4^l), the z pass reads + writes once (2 vol); two spins; plus the volume
-    # build (1), TV (1), aggregation (1) and the accumulator read-modify-write (1)
-    passes = 2 * (2 * sum(4 / 4 ** l for l in range(levels)) + 2) + 4
+    # per spin (fused 2D passes): level-1 analysis writes the 4 subbands (1 vol; the volume is
+    # gathered from the image), levels l >= 2 read + write the band (2 vol / 4^(l-1)), the z
+    # pass reads + writes (2), synthesis mirrors the analysis with level 1 reading the
+    # coefficients and storing U (spin 0: 2) or adding into it (spin 1: 3); then TV + the
+    # aggregation read U once (1)
+    band = sum(2 / 4 ** (l - 1) for l in range(2, levels + 1))
+    passes = (1 + band + 2 + band + 2) + (1 + band + 2 + band + 3) + 1
     nbytes = passes * vol
     peak, src = measured_peak("hbm_gbs", 7672.0)
     ach = nbytes / (ms * 1e-3) / 1e9

@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "match_direct.cuh"
 #include "match_strip.cuh"
+#include "strip_p8s8.cuh"
 #include "match_tc16.cuh"
 
 namespace gbm3d {
@@ -37,6 +38,7 @@ static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* la
         case 1204: return launch_shape<12, 4, 4, 4, 2>(p, st, launches);
         case 802: return launch_shape<8, 2, 8, 5, 2>(p, st, launches);
         case 804: return launch_shape<8, 4, 6, 4, 2>(p, st, launches);
+        case 808: return launch_shape<8, 8, GBM3D_S8_TRY, GBM3D_S8_D, GBM3D_S8_WPS>(p, st, launches);  // stage-1 tiling
         default: *ok = false; return cudaSuccess;
     }
 }

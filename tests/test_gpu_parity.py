@@ -106,7 +106,10 @@ EDGE = [
     (70, 29, 8, 3, 7, 16, None, "uniform"),     # W < 32 reference columns
     (200, 300, 8, 3, 19, 32, None, "uniform"),  # several CTAs x warps, ragged tail
     (60, 70, 8, 9, 19, 16, None, "uniform"),    # stride > patch (direct kernel)
-    (60, 70, 8, 8, 19, 16, None, "uniform"),    # stride = patch (paper tiling, direct)
+    (60, 70, 8, 8, 19, 16, None, "uniform"),    # stride = patch (paper tiling, strip s8)
+    (256, 200, 8, 8, 16, 16, None, "uniform"),  # stage-1 tiling, several strips, ragged
+    (104, 96, 8, 8, 19, 32, 200000, "uniform"), # tiling with tau, K32
+    (72, 88, 8, 8, 16, 16, None, "constant"),   # tiling, pure tie order
     (61, 59, 12, 4, 19, 16, 720000, "uniform"),
     (81, 97, 8, 2, 11, 16, None, "uniform"),
     (81, 97, 8, 4, 19, 24, None, "uniform"),

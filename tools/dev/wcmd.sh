@@ -1,2 +1,13 @@
 mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:s1_(ana_xy|syn_xy)" -c 6 -o gpurun_out/s1_v5 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
+for v in s1_old s8_141 s8_181 s8_282 main; do
+  lib=variants/$v.so; [ $v = main ] && lib=paper_2103_10765_b200/libgbm3d.so
+  GBM3D_LIB=$lib TAG=$v python tools/dev/time_match.py c3 8 8 19 16
+done
+GBM3D_LIB=paper_2103_10765_b200/libgbm3d.so TAG=r16 python tools/dev/time_match.py c3 8 8 16 16
+GBM3D_LIB=variants/s1_old.so TAG=r16old python tools/dev/time_match.py c3 8 8 16 16
+python -c "
+import numpy as np
+for t in ['s8_141','s8_181','s8_282','main']:
+    print(t, all((np.load(f'gpurun_out/m_{t}_{a}.npy')==np.load(f'gpurun_out/m_s1_old_{a}.npy')).all() for a in ('idx','dist')))
+print('r16', all((np.load(f'gpurun_out/m_r16_{a}.npy')==np.load(f'gpurun_out/m_r16old_{a}.npy')).all() for a in ('idx','dist')))
+"
