@@ -295,6 +295,7 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
     line["gather"] = run_gather(args, cfg, call, torch, g, img, outs[0], flush_buf)
     line["wiener"] = run_wiener(args, cfg, call, torch, g, img, outs, flush_buf)
     line["stage1"] = run_stage1(args, cfg, call, torch, g, img, flush_buf)
+    line["denoiser"] = run_denoiser(args, cfg, torch, img, flush_buf)
     if want_e2e:
         line["e2e"] = run_e2e(args, cfg, call, torch, g)
     if want_cpu:
@@ -418,6 +419,36 @@ def run_stage1(args, cfg, call, torch, g, img, flush_buf):
             "ms": ms, "pixels_per_s": cfg.B * cfg.H * cfg.W / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "bytes_per_call": nbytes, "peak_source": src}}
+
+
+def run_denoiser(args, cfg, torch, img, flush_buf):
+    """The whole two-stage G-BM3D (paper_2103_10765_b200.denoise: stage 1 with 3 translation
+    trials of tiling matching + global volume thresholding, stage 2 matching on the basic
+    estimate + Wiener filtering) on the workload's image, single images only.  Context: the
+    paper's Table II times G-BM3D2 on a 2048^2 image at 20.58 s (MATLAB, Titan Xp)."""
+    from paper_2103_10765_b200.denoise import denoise
+    from synth import make_image
+    if cfg.B != 1 or cfg.H % 16 or cfg.W % 16:
+        return None
+    _, clean, sig = make_image(cfg.H, cfg.W, cfg.n_rect, cfg.n_tex, cfg.sigma, cfg.seeds[0],
+                               return_clean=True)
+    out = {}
+
+    def step():
+        out["y"] = denoise(img, sig)
+
+    times = measure_device(step, max(3, args.steps // 4), args.warmup, flush_buf.zero_, torch,
+                           soak_s=0.2)
+    ms = statistics.mean(times)
+    y = out["y"].double().cpu().numpy()
+    noisy = img.double().cpu().numpy()
+    psnr = lambda a: float(10 * np.log10(255.0 ** 2 / np.mean((a - clean) ** 2)))
+    return {"what": "denoise(): G-BM3D2 = stage 1 (3 trials: P8 s8 K16 r16 matching + global "
+                    "volume thresholding) + stage 2 (P8 s3 K32 r16 matching on the basic "
+                    "estimate + Wiener), synthetic image",
+            "ms": ms, "psnr_noisy_db": psnr(noisy), "psnr_out_db": psnr(y),
+            "paper_context": {"G-BM3D2_2048_s": 20.58, "source": "P:324 Table II, MATLAB on a "
+                              "Titan Xp, other images; context only"}}
 
 
 def cfg_sigmas(cfg):
