@@ -311,14 +311,30 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
     int32_t* d_idx = (int32_t*)(ws + ((img_b + 255) & ~(size_t)255));
     int32_t* d_dist = (int32_t*)((char*)d_idx + ((nref * K * 4 + 255) & ~(size_t)255));
     int32_t* d_nv = (int32_t*)((char*)d_dist + ((nref * K * 4 + 255) & ~(size_t)255));
-    // chunk plan: [u0, u1) in images (B > 1) or in reference rows (B = 1, multiples of 16 so
-    // the tensor-core tiles of a chunk are the tiles of the whole call)
+    // chunk plan: [ub[c], ub[c+1]) in images (B > 1) or in reference rows (B = 1, multiples of
+    // 16 so the tensor-core tiles of a chunk are the tiles of the whole call; a short first
+    // chunk so the copies out start early)
+#ifndef GBM3D_HOST_NCH
+#define GBM3D_HOST_NCH 12
+#endif
     const int units = B > 1 ? B : p.Ry;
-    int nch = B > 1 ? std::min(B, 8) : std::min(8, std::max(1, p.Ry / 64));
-    int step = (units + nch - 1) / nch;
-    if (B == 1) step = (step + 15) & ~15;
-    nch = (units + step - 1) / step;
-    if (nch > kMaxChunks) return GBM3D_ERR_ARG;  // unreachable: at most 8 chunks
+    int ub[kMaxChunks + 1];
+    int nch = 0;
+    if (B > 1) {
+        const int n = std::min(B, GBM3D_HOST_NCH), step = (B + n - 1) / n;
+        for (int u = 0; u < B; u += step) ub[nch++] = u;
+    } else {
+        const int first = std::min(units, 32);
+        ub[nch++] = 0;
+        if (first < units) {
+            ub[nch++] = first;
+            const int n = std::max(1, std::min(GBM3D_HOST_NCH - 1, (units - first) / 32));
+            const int step = (((units - first + n - 1) / n) + 15) & ~15;
+            for (int u = first + step; u < units; u += step) ub[nch++] = u;
+        }
+    }
+    ub[nch] = units;
+    if (nch > kMaxChunks) return GBM3D_ERR_ARG;  // unreachable: at most GBM3D_HOST_NCH chunks
     int launches = 0;
     // the library streams start after whatever the caller queued before this call
     if (cudaEventRecord(g_pipe.start, s) != cudaSuccess ||
@@ -326,18 +342,32 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
         cudaStreamWaitEvent(g_pipe.comp2, g_pipe.start, 0) != cudaSuccess ||
         cudaStreamWaitEvent(g_pipe.d2h, g_pipe.start, 0) != cudaSuccess)
         return GBM3D_ERR_CUDA;
-    // pixels in: per image chunk (B > 1) or the whole image (B = 1)
-    for (int c = 0; c < (B > 1 ? nch : 1); ++c) {
-        const int b0 = B > 1 ? c * step : 0, b1 = B > 1 ? std::min(B, b0 + step) : 1;
-        const size_t off = (size_t)b0 * H * W, n = (size_t)(b1 - b0) * H * W * 2;
-        if (cudaMemcpyAsync(d_img + off, h_imgs + off, n, cudaMemcpyHostToDevice, g_pipe.h2d) != cudaSuccess)
-            return GBM3D_ERR_CUDA;
-        if (cudaEventRecord(g_pipe.in[c], g_pipe.h2d) != cudaSuccess) return GBM3D_ERR_CUDA;
+    // pixels in: per image chunk (B > 1) or, for one image, the pixel rows each chunk of
+    // reference rows needs beyond the previous chunk's (its blocks' rows plus the window)
+    {
+        size_t done_rows = 0;
+        for (int c = 0; c < nch; ++c) {
+            size_t off, n;
+            if (B > 1) {
+                off = (size_t)ub[c] * H * W;
+                n = (size_t)(ub[c + 1] - ub[c]) * H * W;
+            } else {
+                const int ylast = std::min((ub[c + 1] - 1) * stride, H - patch);
+                const size_t need = (size_t)std::min(H, ylast + patch + radius);
+                off = done_rows * W;
+                n = need > done_rows ? (need - done_rows) * W : 0;
+                done_rows = std::max(done_rows, need);
+            }
+            if (n && cudaMemcpyAsync(d_img + off, h_imgs + off, n * 2, cudaMemcpyHostToDevice,
+                                     g_pipe.h2d) != cudaSuccess)
+                return GBM3D_ERR_CUDA;
+            if (cudaEventRecord(g_pipe.in[c], g_pipe.h2d) != cudaSuccess) return GBM3D_ERR_CUDA;
+        }
     }
     for (int c = 0; c < nch; ++c) {
-        const int u0 = c * step, u1 = std::min(units, u0 + step);
+        const int u0 = ub[c], u1 = ub[c + 1];
         cudaStream_t cs = (c & 1) ? g_pipe.comp2 : s;
-        if (cudaStreamWaitEvent(cs, g_pipe.in[B > 1 ? c : 0], 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+        if (cudaStreamWaitEvent(cs, g_pipe.in[c], 0) != cudaSuccess) return GBM3D_ERR_CUDA;
         MatchParams q = p;
         size_t r0, nr;  // first reference and reference count of the chunk in the outputs
         if (B > 1) {
@@ -364,10 +394,11 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
         if (cudaMemcpyAsync(h_idx + r0 * K, q.idx, nr * K * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess ||
             cudaMemcpyAsync(h_dist + r0 * K, q.dist, nr * K * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
             return GBM3D_ERR_CUDA;
-        if (h_n_valid &&
-            cudaMemcpyAsync(h_n_valid + r0, q.nvalid, nr * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
-            return GBM3D_ERR_CUDA;
     }
+    // n_valid (small) in one copy after the last chunk
+    if (h_n_valid &&
+        cudaMemcpyAsync(h_n_valid, d_nv, nref * 4, cudaMemcpyDeviceToHost, g_pipe.d2h) != cudaSuccess)
+        return GBM3D_ERR_CUDA;
     g_last_launches = launches;
     // the caller's stream is ordered after the copies out (which follow every chunk's
     // matching), then the call blocks on it

@@ -241,6 +241,29 @@ def test_host_entry_matches_device_entry():
     assert torch.equal(hi, di.cpu()) and torch.equal(hd, dd.cpu()) and torch.equal(hn, dn.cpu())
 
 
+@pytest.mark.parametrize("P,s,r,K", [(8, 3, 19, 32), (8, 8, 16, 16), (12, 4, 19, 16)])
+def test_host_entry_single_image_row_chunks(P, s, r, K):
+    """One large image: the host entry copies the pixels in row bands and matches row chunks
+    (a short first chunk, then equal ones) on two streams; the tables must equal the device
+    entry's on the c3 image, and the oracle's on sampled references."""
+    g = _gbm3d()
+    img = config_images("c3")[0]
+    hi, hd, hn = g.block_match_host(torch.from_numpy(img).pin_memory(), P, s, r, K)
+    di, dd, dn = g.block_match(torch.from_numpy(img).cuda(), P, s, r, K)
+    for a, b in ((hi, di), (hd, dd), (hn, dn)):
+        assert torch.equal(a.reshape(b.shape), b.cpu())
+    # sampled references against the oracle (first and last reference rows, chunk borders)
+    Ry, Rx = di.shape[:2]
+    rng = np.random.default_rng(P * 100 + s)
+    rows = [0, 31, 32, 33, Ry - 1] + list(rng.integers(0, Ry, 3))
+    refs = [(int(y), int(x)) for y in rows for x in (0, Rx - 1, int(rng.integers(0, Rx)))]
+    py, px = np.array(refs).T
+    ei, ed, en = oracle.block_match_refs(img, P, s, r, K, None, py, px)
+    assert np.array_equal(di.cpu().numpy()[py, px], ei)
+    assert np.array_equal(dd.cpu().numpy()[py, px], ed)
+    assert np.array_equal(dn.cpu().numpy()[py, px], en)
+
+
 def test_check_range_and_error_codes():
     g = _gbm3d()
     ok = torch.from_numpy(config_images("c0")[0]).cuda()
