@@ -167,12 +167,21 @@ __global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __rest
         float v[RPW][3];
         if (GATHER) {
             int cpos[RPW][3];
+            if (table) {
+                const int* const tflat = &ttab[0][0];
 #pragma unroll
-            for (int q = 0; q < RPW; ++q) {
-                const int r = min(warp + 8 * q, FIN - 1);
+                for (int q = 0; q < RPW; ++q) {
+                    const int ro = rl[min(warp + 8 * q, FIN - 1)] * NBT;
 #pragma unroll
-                for (int m = 0; m < 3; ++m)
-                    cpos[q][m] = table ? ttab[rl[r]][cq[m]] : __ldg(idx + rl[r] + cq[m]);
+                    for (int m = 0; m < 3; ++m) cpos[q][m] = tflat[ro + cq[m]];
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < RPW; ++q) {
+                    const int ro = rl[min(warp + 8 * q, FIN - 1)];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) cpos[q][m] = __ldg(idx + ro + cq[m]);
+                }
             }
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {

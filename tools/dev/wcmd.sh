@@ -1,2 +1,2 @@
-for v in main; do lib=paper_2103_10765_b200/libgbm3d.so; echo $v; GBM3D_LIB=$lib python tools/dev/time_host.py c3; GBM3D_LIB=$lib python tools/dev/time_host.py c4; done
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "host or row_ranges or batched" 2>&1 | tail -2
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:s1_ana_xy -c 1 -o gpurun_out/s1_ana1 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
