@@ -491,6 +491,24 @@ def run_e2e(args, cfg, call, torch, g):
             "d2h_bytes_per_step": int(sum(o.numel() * 4 for o in out))}
 
 
+def add_multi_roofline(line, cfg, call):
+    """The N-GPU line's ALU roofline, per GPU: the closed-form evaluations over all ranks / N
+    against one GPU's derived INT32 peak, at the max-over-ranks step time (which includes the
+    c3 gather)."""
+    n = line["n_gpus"]
+    ms = line["ms_per_step"]
+    evals1, _ = total_evals(cfg.H, cfg.W, call.patch, call.stride, call.radius)
+    evals = evals1 * cfg.B
+    A = a_eval(call.stride)
+    sm_max = (line.get("clocks") or {}).get("sm_max_mhz") or 1965.0
+    peak = INT_LANES_PER_SM * N_SMS * sm_max * 1e6 / 1e12
+    achieved = evals / n * A / (ms * 1e-3) / 1e12
+    line["gevals_per_s"] = evals / (ms * 1e-3) / 1e9
+    line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TOP/s",
+                        "frac": achieved / peak, "traffic": None, "ops_per_eval": A,
+                        "per": "GPU (evaluations / N over the max-over-ranks step time)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -518,8 +536,10 @@ def main():
     import paper_2103_10765_b200 as g
     if world > 1 or args.gpus > 1:
         from paper_2103_10765_b200 import dist as gdist
-        line = gdist.bench_multi(args, cfg, call)
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        line = gdist.bench_multi(args, cfg, call, sampler=ClockSampler(local))
         if line is not None and rank == 0:
+            add_multi_roofline(line, cfg, call)
             print(json.dumps(line), flush=True)
         return
     torch.cuda.set_device(0)

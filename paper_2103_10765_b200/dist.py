@@ -125,9 +125,95 @@ def _init():
     return rank, world, local
 
 
-def bench_multi(args, cfg, call):
+def _e2e_bytes(cfg, call, Ry, Rx, world):
+    """Bytes per step over all ranks: the slabs (with their halo rows) or images in, the tables
+    out (idx, dist int32 [.., K] and n_valid int32)."""
+    if cfg.B == 1:
+        ranges = row_partition(Ry, world)
+        rows_in = 0
+        for k0, k1 in ranges:
+            y0, y1 = slab_bounds(cfg.H, call.patch, call.stride, call.radius, k0, k1)
+            rows_in += y1 - y0
+        h2d = rows_in * cfg.W * 2
+    else:
+        h2d = cfg.B * cfg.H * cfg.W * 2
+    d2h = cfg.B * Ry * Rx * (2 * call.K + 1) * 4
+    return {"h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+def _e2e_multi(args, cfg, call, g, dev, rank, world, sharded):
+    """Per-step wall time (ms, max over ranks) of host input -> match -> host tables."""
+    from synth import config_images
+    Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
+    if sharded:
+        img = torch.from_numpy(config_images(cfg)[0])
+        k0, k1 = row_partition(Ry, world)[rank]
+        y0, y1 = slab_bounds(cfg.H, call.patch, call.stride, call.radius, k0, k1)
+        h_in = img[y0:y1].contiguous().pin_memory()
+        n_img, rows = 1, k1 - k0
+    else:
+        b0, b1 = batch_partition(cfg.B, world)[rank]
+        h_in = torch.from_numpy(config_images(cfg)[b0:b1]).pin_memory()
+        n_img, rows = b1 - b0, Ry
+    shape = (n_img, rows, Rx) if not sharded else (rows, Rx)
+    h_out = (torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
+             torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
+             torch.empty(shape, dtype=torch.int32, pin_memory=True))
+    d_out = tuple(torch.empty_like(t, device=dev) for t in h_out)
+    ws = None
+    if not sharded:
+        ws = torch.empty(g.host_workspace_bytes(n_img, cfg.H, cfg.W, call.patch, call.stride,
+                                                call.K), dtype=torch.uint8, device=dev)
+
+    d_in = torch.empty(h_in.shape, dtype=h_in.dtype, device=dev)
+    copy_stream = torch.cuda.Stream(device=dev)
+    # row chunks of the rank's range (multiples of 16 rows): the copy of chunk c's tables
+    # overlaps the matching of chunk c + 1
+    nck = max(1, min(6, rows // 32))
+    stepr = ((rows + nck - 1) // nck + 15) // 16 * 16
+    chunks = [(a, min(rows, a + stepr)) for a in range(0, rows, stepr)]
+
+    def step():
+        if sharded:
+            comp = torch.cuda.current_stream(dev)
+            with torch.cuda.stream(copy_stream):
+                d_in.copy_(h_in, non_blocking=True)
+            comp.wait_stream(copy_stream)
+            for a, b in chunks:
+                dv = tuple(t[a:b] for t in d_out)
+                g.block_match_rows(d_in, y0, cfg.H, cfg.W, call.patch, call.stride, call.radius,
+                                   call.K, call.tau, k0 + a, k0 + b, out=dv)
+                copy_stream.wait_stream(comp)
+                with torch.cuda.stream(copy_stream):
+                    for h, d in zip(h_out, dv):
+                        h[a:b].copy_(d, non_blocking=True)
+            copy_stream.synchronize()
+        else:
+            # the pipelined host-buffer entry (copies overlapped with the matching)
+            g.block_match_host(h_in, call.patch, call.stride, call.radius, call.K, call.tau,
+                               workspace=ws, out=h_out)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    dist.barrier()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    t = torch.tensor([1e3 * sum(ts) / len(ts)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bench_multi(args, cfg, call, sampler=None):
     """N-GPU measurement: c3 row-sharded + NCCL gather to rank 0 (timed), c4 batch split
-    (no collective).  Max over ranks of the per-rank device time."""
+    (no collective).  Max over ranks of the per-rank device time.  `sampler` (optional, with
+    start() / stop() / summary()) samples this rank's GPU clocks around the timed region; rank
+    0 reports the lowest median clock and the union of throttle reasons over the ranks.  The
+    end-to-end leg times, per step and on every rank, the pinned-host copy of the rank's input
+    (slab or images), the match and the copy of the rank's tables back to pinned host memory
+    (wall clock, max over ranks)."""
     import paper_2103_10765_b200 as g
     from synth import config_images
 
@@ -174,6 +260,13 @@ def bench_multi(args, cfg, call):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    if sampler is not None:
+        sampler.start()
+        t_end = time.time() + 1.0  # clock soak inside the sampled window
+        while time.time() < t_end:
+            step()
+            torch.cuda.synchronize()
+        dist.barrier()
     stream = torch.cuda.current_stream()
     times = []
     for _ in range(args.steps):
@@ -186,8 +279,16 @@ def bench_multi(args, cfg, call):
         times.append((s, e))
     torch.cuda.synchronize()
     dist.barrier()
+    clocks = None
+    if sampler is not None:
+        sampler.stop()
+        clocks = sampler.summary()
     ms = torch.tensor([sum(s.elapsed_time(e) for s, e in times) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    launches = g.last_launch_count()
+    e2e_ms = _e2e_multi(args, cfg, call, g, dev, rank, world, sharded)
+    all_clocks = [None] * world
+    dist.all_gather_object(all_clocks, clocks)
     total_refs = Ry * Rx * cfg.B
     line = None
     if rank == 0:
@@ -195,13 +296,25 @@ def bench_multi(args, cfg, call):
         line = {"metric": "ref patches matched/sec", "value": total_refs / (t * 1e-3),
                 "unit": "refs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "i32", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f16+i32", "data": "synthetic",
                 "config": {"workload": f"{cfg.name}: {cfg.note}", "H": cfg.H, "W": cfg.W,
                            "B": cfg.B, "patch": call.patch, "stride": call.stride,
                            "radius": call.radius, "K": call.K, "tau": call.tau,
                            "parallelism": ("rows+nccl-gather" if sharded else "batch") +
                            f"x{world}", "l2": "256 MiB write between timed steps"},
-                "gpu_launches": g.last_launch_count() * args.steps,
+                "gpu_launches": launches * args.steps,
                 "rank0_refs": my_refs}
+        if e2e_ms is not None:
+            line["e2e"] = {"value": total_refs / (e2e_ms * 1e-3), "unit": "refs/s",
+                           "ms_per_step": e2e_ms, **_e2e_bytes(cfg, call, Ry, Rx, world),
+                           "note": "per rank: pinned H2D of its input, match, D2H of its "
+                                   "tables; wall clock, max over ranks"}
+        cl = [c for c in all_clocks if c]
+        if cl:
+            mhz = [c["sm_mhz"] for c in cl if c.get("sm_mhz")]
+            line["clocks"] = {"sm_mhz": min(mhz) if mhz else None,
+                              "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in cl) or None,
+                              "reasons": sorted({r for c in cl for r in c.get("reasons", [])}),
+                              "per_rank_sm_mhz": [c.get("sm_mhz") for c in all_clocks if c]}
     dist.destroy_process_group()
     return line
