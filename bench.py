@@ -540,6 +540,8 @@ def main():
         line = gdist.bench_multi(args, cfg, call, sampler=ClockSampler(local))
         if line is not None and rank == 0:
             add_multi_roofline(line, cfg, call)
+            # the same config object as the N = 1 line and the reference arm
+            line["config"] = workload_config(cfg, call, args)
             print(json.dumps(line), flush=True)
         return
     torch.cuda.set_device(0)
