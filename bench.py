@@ -292,6 +292,8 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
         "clocks": clocks,
         "kernel_ms": {"mean": ms, "min": min(times), "max": max(times)},
     }
+    if args.step_only:   # profiling runs: the timed step's kernels alone
+        return line
     line["gather"] = run_gather(args, cfg, call, torch, g, img, outs[0], flush_buf)
     line["wiener"] = run_wiener(args, cfg, call, torch, g, img, outs, flush_buf)
     line["stage1"] = run_stage1(args, cfg, call, torch, g, img, flush_buf)
@@ -519,6 +521,9 @@ def main():
     ap.add_argument("--method", default="auto", choices=["auto", "ssd", "product", "direct"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-also", action="store_true", help="skip the secondary c4 line")
+    ap.add_argument("--step-only", action="store_true",
+                    help="only the timed matching step (no gather / stage legs, e2e, CPU "
+                         "baseline): for ncu launch lists of the step")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
