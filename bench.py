@@ -298,6 +298,8 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
     line["wiener"] = run_wiener(args, cfg, call, torch, g, img, outs, flush_buf)
     line["stage1"] = run_stage1(args, cfg, call, torch, g, img, flush_buf)
     line["denoiser"] = run_denoiser(args, cfg, torch, img, flush_buf)
+    if want_cpu:
+        line["small_configs"] = run_small_configs(torch, g)
     if want_e2e:
         line["e2e"] = run_e2e(args, cfg, call, torch, g)
     if want_cpu:
@@ -451,6 +453,60 @@ def run_denoiser(args, cfg, torch, img, flush_buf):
             "ms": ms, "psnr_noisy_db": psnr(noisy), "psnr_out_db": psnr(y),
             "paper_context": {"G-BM3D2_2048_s": 20.58, "source": "P:324 Table II, MATLAB on a "
                               "Titan Xp, other images; context only"}}
+
+
+def run_small_configs(torch, g):
+    """the latency of the small configs c0-c2 (parity cases) at 1 GPU: device
+    time per call (CUDA events around 50 back-to-back calls, after warm-up), and the same call
+    replayed from a captured CUDA graph (launch overhead removed)."""
+    from synth import CONFIGS, config_images
+    res = {}
+    for name in ("c0", "c1", "c2"):
+        cfg = CONFIGS[name]
+        img = torch.from_numpy(config_images(cfg)[0]).cuda()
+        for ci, call in enumerate(cfg.calls):
+            Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
+            outs = (torch.empty((Ry, Rx, call.K), dtype=torch.int32, device="cuda"),
+                    torch.empty((Ry, Rx, call.K), dtype=torch.int32, device="cuda"),
+                    torch.empty((Ry, Rx), dtype=torch.int32, device="cuda"))
+
+            def step():
+                g.block_match(img, call.patch, call.stride, call.radius, call.K, call.tau,
+                              check=False, out=outs)
+
+            for _ in range(10):
+                step()
+            torch.cuda.synchronize()
+            reps = 50
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(reps):
+                step()
+            e.record()
+            torch.cuda.synchronize()
+            us = 1e3 * s.elapsed_time(e) / reps
+            launches = g.last_launch_count()
+            graph_us = None
+            try:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr):
+                    step()
+                for _ in range(5):
+                    gr.replay()
+                torch.cuda.synchronize()
+                s.record()
+                for _ in range(reps):
+                    gr.replay()
+                e.record()
+                torch.cuda.synchronize()
+                graph_us = 1e3 * s.elapsed_time(e) / reps
+            except Exception as exc:  # capture unsupported: report it, keep the eager number
+                graph_us = f"capture failed: {type(exc).__name__}"
+            res[f"{name}.call{ci}"] = {"us_per_call": us, "graph_us_per_call": graph_us,
+                                       "refs": Ry * Rx, "refs_per_s": Ry * Rx / (us * 1e-6),
+                                       "launches": launches, "P": call.patch, "s": call.stride,
+                                       "K": call.K, "tau": call.tau}
+    return res
 
 
 def cfg_sigmas(cfg):

@@ -10,6 +10,7 @@
 #include "match_direct.cuh"
 #include "match_strip.cuh"
 #include "strip_p8s8.cuh"
+#include "strip_p12s4.cuh"
 #include "match_tc16.cuh"
 
 namespace gbm3d {
@@ -35,7 +36,7 @@ static cudaError_t strip_dispatch(const MatchParams& p, cudaStream_t st, int* la
     *ok = true;
     switch (p.P * 100 + p.S) {
         case 803: return launch_shape<8, 3, 4, 8, 1>(p, st, launches);     // solo warps
-        case 1204: return launch_shape<12, 4, 4, 4, 2>(p, st, launches);
+        case 1204: return launch_shape<12, 4, GBM3D_S12_TRY, GBM3D_S12_D, GBM3D_S12_WPS>(p, st, launches);
         case 802: return launch_shape<8, 2, 8, 5, 2>(p, st, launches);
         case 804: return launch_shape<8, 4, 6, 4, 2>(p, st, launches);
         case 808: return launch_shape<8, 8, GBM3D_S8_TRY, GBM3D_S8_D, GBM3D_S8_WPS>(p, st, launches);  // stage-1 tiling
@@ -132,10 +133,36 @@ static int cuda_fail(cudaError_t e, const char* where) {
     return GBM3D_ERR_CUDA;
 }
 
+// Two library-owned side streams per host thread for the direct kernel's appended row and
+// column: they depend only on the inputs, so they fork from the caller's stream before the
+// fast kernel and join after it (the three run concurrently; capturable in CUDA graphs).
+struct SideStreams {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    bool ok = false, tried = false;
+    bool init() {
+        if (tried) return ok;
+        tried = true;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking) != cudaSuccess) return false;
+            if (cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming) != cudaSuccess) return false;
+        }
+        if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return false;
+        ok = true;
+        return true;
+    }
+};
+static thread_local SideStreams g_side;
+
 static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
     bool fast = false;
+    const int kr1_ = std::min(p.row_end, p.Ry_reg);
+    const bool app_col = p.Rx > p.Rx_reg && kr1_ > p.row_begin;
+    const bool app_row = p.Ry > p.Ry_reg && p.row_end > p.Ry_reg;
+    const bool side = method != GBM3D_METHOD_DIRECT && (app_col || app_row) && g_side.init();
+    if (side && cudaEventRecord(g_side.fork, st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fork");
     if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_PRODUCT ||
         method == GBM3D_METHOD_PRODUCT_I8) {
         // AUTO prefers the tensor-core product form (fastest where it applies)
@@ -149,12 +176,22 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
         if (!fast && method == GBM3D_METHOD_SSD) return GBM3D_ERR_UNSUPPORTED;
     }
     if (fast) {
-        const int kr1 = std::min(p.row_end, p.Ry_reg);
-        // appended column for the regular rows of the call
-        if (p.Rx > p.Rx_reg) e = launch_direct(p, st, p.row_begin, kr1, p.Rx_reg, p.Rx, &launches);
-        // appended row (all columns) when it is inside the call's row range
-        if (e == cudaSuccess && p.Ry > p.Ry_reg && p.row_end > p.Ry_reg)
-            e = launch_direct(p, st, std::max(p.row_begin, p.Ry_reg), p.row_end, 0, p.Rx, &launches);
+        const int kr1 = kr1_;
+        // appended column for the regular rows of the call, appended row (all columns) when it
+        // is inside the call's row range: on the side streams when available
+        cudaStream_t sc = side ? g_side.s[0] : st, sr = side ? g_side.s[1] : st;
+        if (app_col) {
+            if (side && cudaStreamWaitEvent(sc, g_side.fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+            e = launch_direct(p, sc, p.row_begin, kr1, p.Rx_reg, p.Rx, &launches);
+            if (e == cudaSuccess && side) e = cudaEventRecord(g_side.join[0], sc);
+            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, g_side.join[0], 0);
+        }
+        if (e == cudaSuccess && app_row) {
+            if (side && cudaStreamWaitEvent(sr, g_side.fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+            e = launch_direct(p, sr, std::max(p.row_begin, p.Ry_reg), p.row_end, 0, p.Rx, &launches);
+            if (e == cudaSuccess && side) e = cudaEventRecord(g_side.join[1], sr);
+            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, g_side.join[1], 0);
+        }
     } else {
         e = launch_direct(p, st, p.row_begin, p.row_end, 0, p.Rx, &launches);
     }
