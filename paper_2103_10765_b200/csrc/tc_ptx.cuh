@@ -54,11 +54,16 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
 #ifndef GBM3D_TC_SPIN
 #define GBM3D_TC_SPIN 0
 #endif
+#ifndef GBM3D_TC_SLEEP_NS
+#define GBM3D_TC_SLEEP_NS 32
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    if (GBM3D_TC_SPIN) {
+    if (GBM3D_TC_SPIN == 1) {
         while (!mbar_try_wait(a, parity)) {
         }
+    } else if (GBM3D_TC_SPIN == 2) {  // dev experiment: polling with a short sleep backoff
+        while (!mbar_try_wait(a, parity)) __nanosleep(GBM3D_TC_SLEEP_NS);
     } else {
         while (!mbar_try_wait_sleep(a, parity)) {
         }
