@@ -235,14 +235,11 @@ extern "C" int gbm3d_gather_groups(const int16_t* imgs, int B, int H, int W, int
         const int chmax = SLOTS / K < 128 ? SLOTS / K : 128;
         const int nchunk = (Rx + chmax - 1) / chmax;
         const int ch = (Rx + nchunk - 1) / nchunk;
-        static bool attr = false;
-        if (!attr) {
-            if (cudaFuncSetAttribute(gather_groups8_tiled_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     GATHER_SMEM) != cudaSuccess)
-                return GBM3D_ERR_CUDA;
-            attr = true;
-        }
+        // per call: the attribute is per device, and the call may come from any thread
+        if (cudaFuncSetAttribute(gather_groups8_tiled_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GATHER_SMEM) != cudaSuccess)
+            return GBM3D_ERR_CUDA;
         dim3 grid((unsigned)(Ry * ((Rx + ch - 1) / ch)), (unsigned)B);
         gather_groups8_tiled_kernel<<<grid, 256, GATHER_SMEM, s>>>(
             imgs, H, W, idx, Ry, Rx, K, ch, reinterpret_cast<uint4*>(groups));

@@ -319,13 +319,10 @@ cudaError_t launch_wiener(const int16_t* noisy, const float* basic, int B, int H
                           const int32_t* idx, const int32_t* nvalid, int Ry, int Rx,
                           const float* sigmas, float* num, float* wmap, cudaStream_t s) {
     const int smem = WIENER_SMEM;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(wiener_tile_kernel<K>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // per call: the attribute is per device, and the call may come from any thread
+    cudaError_t e = cudaFuncSetAttribute(wiener_tile_kernel<K>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((Rx + WT - 1) / WT), (unsigned)((Ry + WT - 1) / WT), (unsigned)B);
     wiener_tile_kernel<K><<<grid, WTHREADS, smem, s>>>(noisy, basic, H, W, idx, nvalid, Ry, Rx,
                                                        sigmas, num, wmap);
