@@ -185,8 +185,9 @@ int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch, c
  * and BLOCKS until the results are on the host.  The work is pipelined in up to 12 chunks
  * (images for B > 1; for B = 1 blocks of reference rows -- a 32-row first chunk, then equal
  * multiples of 16 -- whose pixel rows are copied in as bands): copies run on two
- * library-owned streams (created once per host thread) overlapped with the matching on
- * `stream` and a second library stream; n_valid comes back in one copy at the end.
+ * library-owned streams (created once per host thread and device) overlapped with the
+ * matching on `stream` and a second library stream; n_valid comes back in one copy at the
+ * end.
  * Results are identical to the device entries. */
 size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, int K);
 int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,

@@ -152,7 +152,15 @@ struct SideStreams {
         return true;
     }
 };
-static thread_local SideStreams g_side;
+// one set per (host thread, device): library streams belong to the device current at creation
+constexpr int kMaxDevices = 16;
+static thread_local SideStreams g_side_dev[kMaxDevices];
+static SideStreams* side_for_current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    SideStreams* sd = &g_side_dev[dev];
+    return sd->init() ? sd : nullptr;
+}
 
 static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
@@ -161,8 +169,10 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
     const int kr1_ = std::min(p.row_end, p.Ry_reg);
     const bool app_col = p.Rx > p.Rx_reg && kr1_ > p.row_begin;
     const bool app_row = p.Ry > p.Ry_reg && p.row_end > p.Ry_reg;
-    const bool side = method != GBM3D_METHOD_DIRECT && (app_col || app_row) && g_side.init();
-    if (side && cudaEventRecord(g_side.fork, st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fork");
+    SideStreams* const sd =
+        (method != GBM3D_METHOD_DIRECT && (app_col || app_row)) ? side_for_current_device() : nullptr;
+    const bool side = sd != nullptr;
+    if (side && cudaEventRecord(sd->fork, st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "fork");
     if (method == GBM3D_METHOD_AUTO || method == GBM3D_METHOD_PRODUCT ||
         method == GBM3D_METHOD_PRODUCT_I8) {
         // AUTO prefers the tensor-core product form (fastest where it applies)
@@ -179,18 +189,18 @@ static int run(const MatchParams& p, int method, cudaStream_t st) {
         const int kr1 = kr1_;
         // appended column for the regular rows of the call, appended row (all columns) when it
         // is inside the call's row range: on the side streams when available
-        cudaStream_t sc = side ? g_side.s[0] : st, sr = side ? g_side.s[1] : st;
+        cudaStream_t sc = side ? sd->s[0] : st, sr = side ? sd->s[1] : st;
         if (app_col) {
-            if (side && cudaStreamWaitEvent(sc, g_side.fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+            if (side && cudaStreamWaitEvent(sc, sd->fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
             e = launch_direct(p, sc, p.row_begin, kr1, p.Rx_reg, p.Rx, &launches);
-            if (e == cudaSuccess && side) e = cudaEventRecord(g_side.join[0], sc);
-            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, g_side.join[0], 0);
+            if (e == cudaSuccess && side) e = cudaEventRecord(sd->join[0], sc);
+            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, sd->join[0], 0);
         }
         if (e == cudaSuccess && app_row) {
-            if (side && cudaStreamWaitEvent(sr, g_side.fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
+            if (side && cudaStreamWaitEvent(sr, sd->fork, 0) != cudaSuccess) return GBM3D_ERR_CUDA;
             e = launch_direct(p, sr, std::max(p.row_begin, p.Ry_reg), p.row_end, 0, p.Rx, &launches);
-            if (e == cudaSuccess && side) e = cudaEventRecord(g_side.join[1], sr);
-            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, g_side.join[1], 0);
+            if (e == cudaSuccess && side) e = cudaEventRecord(sd->join[1], sr);
+            if (e == cudaSuccess && side) e = cudaStreamWaitEvent(st, sd->join[1], 0);
         }
     } else {
         e = launch_direct(p, st, p.row_begin, p.row_end, 0, p.Rx, &launches);
@@ -303,7 +313,8 @@ size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, in
 // overlap on the SMs, so no chunk ends on a partial wave), and the device-to-host copies of
 // chunk c on a third stream while later chunks are matched.  PCIe is full duplex, so
 // the copies hide behind each other and behind the kernels.  The library streams and events
-// are created once per host thread (thread_local) and reused; nothing else is allocated.
+// are created once per host thread and device (thread_local) and reused; nothing else is
+// allocated.
 namespace {
 constexpr int kMaxChunks = 16;
 struct HostPipe {
@@ -325,7 +336,7 @@ struct HostPipe {
         return true;
     }
 };
-thread_local HostPipe g_pipe;
+thread_local HostPipe g_pipe_dev[kMaxDevices];
 }  // namespace
 
 int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch, int stride,
@@ -338,6 +349,9 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
     MatchParams p;
     int st = make_params(p, B, H, W, patch, stride, radius, K, tau);
     if (st != GBM3D_OK) return st;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return GBM3D_ERR_CUDA;
+    HostPipe& g_pipe = g_pipe_dev[dev];
     if (!g_pipe.init()) return GBM3D_ERR_CUDA;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
