@@ -35,9 +35,13 @@
  *
  * Ownership: the caller allocates and owns every buffer.  Device entries take DEVICE
  * pointers and enqueue on `stream` (a cudaStream_t passed as void*; NULL = legacy default
- * stream); they return after enqueueing (results are ready when the stream is).  They hold
- * no state, allocate nothing, and are reentrant: any number of concurrent calls on distinct
- * streams is allowed.  Outputs are undefined after any error.
+ * stream); they return after enqueueing (results are ready when the stream is).  They
+ * allocate no memory and are reentrant: any number of concurrent calls on distinct streams is
+ * allowed.  The only library state is a pair of side streams per host thread and device
+ * (created on first use): a call whose grid has an appended last row / column runs those
+ * references' direct kernel there, forked from and joined back into `stream` with events (so
+ * the call stays ordered on `stream` and is capturable in a CUDA graph).  Outputs are
+ * undefined after any error.
  *
  * Precondition (exactness domain, reading R10): P^2 * (max(Z) - min(Z))^2 <=
  * 2^31 - 1, so every distance fits int32.  gbm3d_check_range verifies it; the device entries
