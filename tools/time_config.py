@@ -1,5 +1,5 @@
-"""Quick device timing of one config (CUDA events, L2 flushed between reps) and optional
-bit-exact check against the oracle on sampled references.  Dev tool, not the bench."""
+"""Quick device timing of one config (CUDA events, L2 flushed between reps).  Dev tool, not the
+bench; parity checks live in tests/."""
 import argparse
 import os
 import sys
@@ -14,7 +14,6 @@ from synth import CONFIGS, config_images  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=10)
-ap.add_argument("--check", type=int, default=0, help="sampled refs to check vs oracle")
 ap.add_argument("--method", default="auto")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
@@ -36,17 +35,3 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     ts.append(s.elapsed_time(e))
 print(f"{a.config} {os.environ.get('GBM3D_STRIP_SOLO', '0')} median {np.median(ts):.3f} ms  min {min(ts):.3f}")
-if a.check:
-    import oracle
-    idx, dist, nv = [t.cpu().numpy() for t in out]
-    if cfg.B == 1:
-        idx, dist, nv = idx[None], dist[None], nv[None]
-    rng = np.random.default_rng(0)
-    bad = 0
-    for b in range(min(cfg.B, 4)):
-        py = rng.integers(0, idx.shape[1], a.check)
-        px = rng.integers(0, idx.shape[2], a.check)
-        ei, ed, en = oracle.block_match_refs(imgs_np[b], c.patch, c.stride, c.radius, c.K, c.tau, py, px)
-        bad += int((ei != idx[b, py, px]).any(-1).sum() + (ed != dist[b, py, px]).any(-1).sum()
-                   + (en != nv[b, py, px]).sum())
-    print("check", "OK" if bad == 0 else f"MISMATCH {bad}")
