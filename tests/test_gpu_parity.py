@@ -306,3 +306,33 @@ def test_fuzz_wide():
             img = special_image("uniform", H, W, seed=case, lo=-150, hi=400)
         _assert_same(_gpu(img, P, s, r, K, tau), oracle.block_match(img, P, s, r, K, tau),
                      f"wide fuzz {case}: {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
+
+
+@pytest.mark.parametrize("name,ci", [("c0", 0), ("c1", 1), ("c2", 0)])
+def test_cuda_graph_replay_matches_oracle(name, ci):
+    """The device entry is capturable in a CUDA graph, including the side streams of the
+    appended row / column (fork / join with events); replays on new pixels give the oracle's
+    tables."""
+    g = _gbm3d()
+    cfg = CONFIGS[name]
+    c = cfg.calls[ci]
+    img = config_images(cfg)[0]
+    t = torch.from_numpy(img).cuda()
+    Ry, Rx = g.grid_dims(cfg.H, cfg.W, c.patch, c.stride)
+    outs = (torch.empty((Ry, Rx, c.K), dtype=torch.int32, device="cuda"),
+            torch.empty((Ry, Rx, c.K), dtype=torch.int32, device="cuda"),
+            torch.empty((Ry, Rx), dtype=torch.int32, device="cuda"))
+    g.block_match(t, c.patch, c.stride, c.radius, c.K, c.tau, check=False, out=outs)  # warm-up
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        g.block_match(t, c.patch, c.stride, c.radius, c.K, c.tau, check=False, out=outs)
+    img2 = np.ascontiguousarray(img[::-1, ::-1])     # new pixels, same shape
+    t.copy_(torch.from_numpy(img2))
+    for o in outs:
+        o.fill_(-7)
+    graph.replay()
+    torch.cuda.synchronize()
+    got = tuple(o.cpu().numpy() for o in outs)
+    _assert_same(got, oracle.block_match(img2, c.patch, c.stride, c.radius, c.K, c.tau),
+                 f"graph replay {name} call {ci}")
