@@ -493,12 +493,16 @@ __device__ __forceinline__ void s1_split(int e, int N, int NN, bool p2, int lg, 
     }
 }
 
+// NC, KC: compile-time N and K (0 = the runtime values), so the common shapes get constant
+// index arithmetic and fully unrolled loops
+template <int NC, int KC>
 __global__ void __launch_bounds__(512) s1_tv_aggregate_kernel(const float* __restrict__ U,
-        const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid, int K, int H, int W,
-        int N, float* __restrict__ num, float* __restrict__ wmap) {
+        const int32_t* __restrict__ idx, const int32_t* __restrict__ nvalid, int K_rt, int H, int W,
+        int N_rt, float* __restrict__ num, float* __restrict__ wmap) {
     extern __shared__ float gsm[];              // [K][N][N], 32 partial sums, K positions
+    const int N = NC > 0 ? NC : N_rt, K = KC > 0 ? KC : K_rt;
     const int Bx = W / N, By = H / N;
-    const int t = threadIdx.x, nt = blockDim.x;
+    const int t = threadIdx.x, nt = (NC > 0 && KC > 0) ? NC * KC : (int)blockDim.x;
     const int g = blockIdx.x, b = blockIdx.y;
     const int p = g / Bx, q = g - p * Bx;
     const int64_t gi = (int64_t)b * By * Bx + g;
@@ -554,8 +558,10 @@ __global__ void __launch_bounds__(512) s1_tv_aggregate_kernel(const float* __res
 
 // out = num / (N x N box sums of the weight map over [y-N+1, y] x [x-N+1, x]): 32 x 32 output
 // tiles, the map staged with its (N-1)-pixel halo, separable sums
+template <int NC>  // compile-time N (0 = runtime)
 __global__ void __launch_bounds__(256) s1_divide_kernel(const float* __restrict__ num,
-        const float* __restrict__ wmap, float* __restrict__ out, int H, int W, int N) {
+        const float* __restrict__ wmap, float* __restrict__ out, int H, int W, int N_rt) {
+    const int N = NC > 0 ? NC : N_rt;
     __shared__ float m[47][48];
     __shared__ float hs[47][33];
     const int b = blockIdx.z, y0 = blockIdx.y * 32, x0 = blockIdx.x * 32;
@@ -668,10 +674,20 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
     {
         const int nt = K * patch;
         const size_t smem = ((size_t)K * patch * patch + 32 + K) * sizeof(float);
-        s1_tv_aggregate_kernel<<<dim3((unsigned)((H / patch) * (W / patch)), B), nt, smem, s>>>(
-            U, idx, n_valid, K, H, W, patch, num, wmap);
+        const dim3 grid((unsigned)((H / patch) * (W / patch)), B);
+        if (patch == 8 && K == 16)
+            s1_tv_aggregate_kernel<8, 16><<<grid, nt, smem, s>>>(U, idx, n_valid, K, H, W, patch, num, wmap);
+        else if (patch == 8 && K == 32)
+            s1_tv_aggregate_kernel<8, 32><<<grid, nt, smem, s>>>(U, idx, n_valid, K, H, W, patch, num, wmap);
+        else
+            s1_tv_aggregate_kernel<0, 0><<<grid, nt, smem, s>>>(U, idx, n_valid, K, H, W, patch, num, wmap);
     }
-    s1_divide_kernel<<<dim3((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), B), 256, 0, s>>>(
-        num, wmap, out, H, W, patch);
+    {
+        const dim3 dg((unsigned)((W + 31) / 32), (unsigned)((H + 31) / 32), B);
+        if (patch == 8)
+            s1_divide_kernel<8><<<dg, 256, 0, s>>>(num, wmap, out, H, W, patch);
+        else
+            s1_divide_kernel<0><<<dg, 256, 0, s>>>(num, wmap, out, H, W, patch);
+    }
     return cudaGetLastError() == cudaSuccess ? GBM3D_OK : GBM3D_ERR_CUDA;
 }
