@@ -183,13 +183,17 @@ __global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __rest
                     for (int m = 0; m < 3; ++m) cpos[q][m] = __ldg(idx + ro + cq[m]);
                 }
             }
+            // last column of a lane: lane + 64 < 73 only for lanes 0..8; rows: warp + 8 q < 73
+            const bool m2ok = lane + 64 < FIN;
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {
                 const int r = warp + 8 * q;
-#pragma unroll
-                for (int m = 0; m < 3; ++m)
-                    if (r < FIN && lane + 32 * m < FIN)
-                        v[q][m] = (float)__ldg(zimg + cpos[q][m] + rtab[r] + cofs[m]);
+                if (q < RPW - 1 || r < FIN) {
+                    const int16_t* const rp = zimg + rtab[r];
+                    v[q][0] = (float)__ldg(rp + (cpos[q][0] + cofs[0]));
+                    v[q][1] = (float)__ldg(rp + (cpos[q][1] + cofs[1]));
+                    if (m2ok) v[q][2] = (float)__ldg(rp + (cpos[q][2] + cofs[2]));
+                }
             }
         } else {
 #pragma unroll
@@ -259,10 +263,13 @@ __global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __rest
             if (m == 2) S2 = x0 + x1;
             if (m == 3) S3 = x0 + x1;
         }
-        float* const lo_base = dcol ? det + (int64_t)s * plane : ll_dst + (int64_t)s * plane + (int64_t)ll_row0 * W;
-        float* const hi_base = det + (int64_t)s * plane;
         const int xo = dcol ? wh + j0 + j : j0 + j;
         const bool colok = j0 + j < wh;
+        // output pointers of this item's first row, advanced by one image row per output
+        float* lo = (dcol ? det + (int64_t)s * plane : ll_dst + (int64_t)s * plane + (int64_t)ll_row0 * W) +
+                    (int64_t)(i0 + ib) * W + xo;
+        float* hi = det + (int64_t)s * plane + (int64_t)(hh + i0 + ib) * W + xo;
+        const int nrow = colok ? min(8, hh - i0 - ib) : 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = ib + u;
@@ -271,10 +278,12 @@ __global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __rest
             const float S4 = x0 + x1;
             float a, d;
             ana_step(D, S2, a, d);
-            if (colok && i0 + i < hh) {
-                lo_base[(int64_t)(i0 + i) * W + xo] = a;
-                hi_base[(int64_t)(hh + i0 + i) * W + xo] = d;
+            if (u < nrow) {
+                *lo = a;
+                *hi = d;
             }
+            lo += W;
+            hi += W;
 #pragma unroll
             for (int t = 0; t < 4; ++t) D[t] = D[t + 1];
             S2 = S3;

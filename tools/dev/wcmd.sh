@@ -1,3 +1,2 @@
-for rep in 1 2; do
-for v in main sleep_20 sleep_64 sleep_128; do lib=variants/$v.so; [ $v = main ] && lib=paper_2103_10765_b200/libgbm3d.so; echo -n "$v "; GBM3D_LIB=$lib python tools/time_config.py --config c3 --reps 20; echo -n "$v "; GBM3D_LIB=$lib python tools/time_config.py --config c4 --reps 10; done
-done
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:s1_ana_xy -c 1 -o gpurun_out/s1_ana1 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
