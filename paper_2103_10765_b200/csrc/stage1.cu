@@ -323,16 +323,17 @@ __global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __rest
 #pragma unroll
         for (int m = 0; m < 3; ++m) cofs[m] = ctab[min(lane + 32 * m, SYN_IN - 1)];
         float v[RPW][3];
+        // column lane (< 32: the LL block for the first 32 rows), lane + 32, lane + 64 (< 68)
+        const bool m2ok = lane + 64 < SYN_IN;
 #pragma unroll
         for (int q = 0; q < RPW; ++q) {
             const int r = warp + 8 * q;
-            if (r < SYN_IN) {
+            if (q < RPW - 1 || r < SYN_IN) {
                 const int64_t ro = (int64_t)rtab[r] * W;
-#pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    const int c = lane + 32 * m;
-                    if (c < SYN_IN) v[q][m] = __ldg(((r < FT && c < FT) ? llp : dp) + ro + cofs[m]);
-                }
+                const float* const rd = dp + ro;
+                v[q][0] = __ldg((r < FT ? llp + ro : rd) + cofs[0]);
+                v[q][1] = __ldg(rd + cofs[1]);
+                if (m2ok) v[q][2] = __ldg(rd + cofs[2]);
             }
         }
 #pragma unroll
@@ -411,21 +412,20 @@ __global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __rest
         const int kk = k >= shift ? k - shift : k - shift + K;
         const int xs = x >= shift ? x - shift : x - shift + W;
         float* const o = dst + (int64_t)(b * K + kk) * plane + xs;
-        int64_t ofs[RPT];
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const int y = y0 + (tid >> 6) + q * (FTHREADS / 64);
-            const int ys = y >= shift ? y - shift : y - shift + H;
-            ofs[q] = (int64_t)ys * W;
-        }
+        // row y = y0 + (tid >> 6) + 4 q lands at y - shift (only y < shift wraps, to y - shift + H)
+        const int yb = y0 + (tid >> 6);
+        auto orow = [&](int q) {
+            const int y = yb + q * (FTHREADS / 64);
+            return o + (int64_t)(y >= shift ? y - shift : y - shift + H) * W;
+        };
         float old[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
-            old[q] = (accumulate == 2 && y0 + (tid >> 6) + q * (FTHREADS / 64) < h) ? o[ofs[q]] : 0.f;
+            old[q] = (accumulate == 2 && yb + q * (FTHREADS / 64) < h) ? *orow(q) : 0.f;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int r = (tid >> 6) + q * (FTHREADS / 64);
-            if (y0 + r < h) o[ofs[q]] = fmaf(scale, out[r][c], old[q]);
+            if (y0 + r < h) *orow(q) = fmaf(scale, out[r][c], old[q]);
         }
     }
 }
