@@ -94,3 +94,17 @@ def test_stage1_batched_and_errors():
         t = oracle.block_match(n, 6, 6, 8, 16, None)
         g.stage1_denoise(torch.from_numpy(n).cuda(), torch.from_numpy(t[0]).cuda(),
                          torch.from_numpy(t[2]).cuda(), 6, 20.0)
+
+
+def test_stage1_full_size_identity():
+    """BASELINE c3's full size (2048^2, tiling N8, K16), through a property that holds at any
+    size: at sigma = 0 nothing is thresholded, every filtered group is its own blocks, and the
+    aggregation returns the noisy image (up to fp32 rounding)."""
+    from synth import config_images
+    g = _g()
+    img = config_images("c3")[0]
+    z = torch.from_numpy(img).cuda()
+    idx, dist, nv = g.block_match(z, 8, 8, 16, 16, None)
+    out = g.stage1_denoise(z, idx, nv, 8, 0.0)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), img.astype(np.float64), atol=1e-2, rtol=0)

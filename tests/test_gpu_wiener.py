@@ -79,3 +79,42 @@ def test_wiener_errors():
     t = lambda a: torch.from_numpy(a).cuda()
     with pytest.raises(g.GBM3DError):  # K = 6 is not a power of two
         g.wiener_stage2(t(noisy), t(basic), t(np.ascontiguousarray(idx[..., :6])), t(nv), 8, sig)
+
+
+def test_wiener_full_size_c3_sampled():
+    """BASELINE c3's full size (2048^2, P8 s3 r19 K32, groups matched on the clean stand-in of
+    the basic estimate by the oracle): the GPU call on the whole image, checked on sampled
+    pixels whose value the oracle rebuilds from every group covering them (wiener_group of
+    each, the aggregation of PAPER.md:190 restricted to the pixel)."""
+    cfg = CONFIGS["c3"]
+    c = cfg.calls[0]
+    noisy, clean, sig = make_image(cfg.H, cfg.W, cfg.n_rect, cfg.n_tex, cfg.sigma, cfg.seeds[0],
+                                   return_clean=True)
+    idx, dist, nv = oracle.block_match(clean, c.patch, c.stride, c.radius, c.K, c.tau)
+    got = _gpu(noisy, clean.astype(np.float32), idx, nv, sig)
+    H, W = noisy.shape
+    N, S, r = c.patch, c.stride, c.radius
+    gy = oracle.grid(H, N, S)
+    gx = oracle.grid(W, N, S)
+    rng = np.random.default_rng(7)
+    pix = [(0, 0), (H - 1, W - 1), (1000, 3)] + [tuple(int(v) for v in rng.integers(0, H, 2)) for _ in range(3)]
+    basic = clean.astype(np.float64)
+    for (y, x) in pix:
+        num = den = 0.0
+        ys = [i for i, v in enumerate(gy) if abs(v - y) <= r + N]
+        xs = [j for j, v in enumerate(gx) if abs(v - x) <= r + N]
+        for i in ys:
+            for j in xs:
+                cy, cx = idx[i, j] // W, idx[i, j] % W
+                ks = [k for k in range(int(nv[i, j]))
+                      if cy[k] <= y < cy[k] + N and cx[k] <= x < cx[k] + N]
+                if not ks:
+                    continue
+                Gz = np.stack([noisy[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
+                Gb = np.stack([basic[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
+                U, w = wiener.wiener_group(Gz, Gb, sig)
+                for k in ks:
+                    num += w * U[k, y - cy[k], x - cx[k]]
+                    den += w
+        assert den > 0
+        assert abs(got[y, x] - num / den) < ATOL, (y, x, got[y, x], num / den)
