@@ -626,20 +626,31 @@ __global__ void __launch_bounds__(tcm::THREADS, 1) match_tc_kernel(MatchParams p
         tc_tile<S, KL>(p, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z);
         return;
     }
-    __shared__ int marked;
+    // every thread checks one tile's flag (tiles interleaved over the CTAs), the marked ones
+    // are collected in shared memory and recomputed by the whole CTA: one flag-load latency
+    // per pass instead of one per tile
+    __shared__ int nmk;
+    __shared__ int mk[tcm::THREADS];
     const int kr1 = min(p.row_end, p.Ry_reg);
     const int nx = (p.Rx_reg + tcm::TX - 1) / tcm::TX, ny = (kr1 - p.row_begin + tcm::TY - 1) / tcm::TY;
     const int total = nx * ny * p.B;
-    for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
-        const int bx = t % nx, by = (t / nx) % ny, bz = t / (nx * ny);
-        if (threadIdx.x == 0) {
+    const int stride = (int)gridDim.x * (int)blockDim.x;
+    for (int t0 = (int)blockIdx.x; t0 < total; t0 += stride) {
+        if (threadIdx.x == 0) nmk = 0;
+        __syncthreads();
+        const int t = t0 + (int)threadIdx.x * (int)gridDim.x;
+        if (t < total) {
+            const int bx = t % nx, by = (t / nx) % ny, bz = t / (nx * ny);
             const int64_t ref = (int64_t)bz * p.out_bstride + (int64_t)(by * tcm::TY) * p.Rx + bx * tcm::TX;
-            marked = p.dist[ref * p.K] == TC_TILE_MARK;
+            if (p.dist[ref * p.K] == TC_TILE_MARK) mk[atomicAdd(&nmk, 1)] = t;
         }
         __syncthreads();
-        const bool m = marked != 0;
+        const int n = nmk;
+        for (int i = 0; i < n; ++i) {
+            const int tt = mk[i];
+            tc_tile<S, KL>(p, tt % nx, (tt / nx) % ny, tt / (nx * ny));
+        }
         __syncthreads();
-        if (m) tc_tile<S, KL>(p, bx, by, bz);
     }
 }
 

@@ -1,2 +1,11 @@
-mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:s1_ana_xy -c 1 -o gpurun_out/s1_ana1 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
+for i in 1 2; do python tools/time_config.py --config c3 --reps 20; python tools/time_config.py --config c4 --reps 10; done
+python -c "
+import torch, paper_2103_10765_b200 as g
+from paper_2103_10765_b200.denoise import denoise
+img = torch.randint(0, 255, (512, 512), dtype=torch.int16, device='cuda')
+idx, dist, n_valid = g.block_match(img, patch=8, stride=3, radius=19, K=16)
+groups = g.gather_groups(img, idx, 8)
+y = denoise(img, sigma=25.0)
+torch.cuda.synchronize(); print('readme ok', tuple(groups.shape), tuple(y.shape), y.dtype)
+"
