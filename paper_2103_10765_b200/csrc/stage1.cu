@@ -9,15 +9,14 @@
 // aggregated with weights 1 / TV (3D total variation), the pad blocks left
 // out.  Readings S1-S7 in DESIGN.md.
 //
-// Layout: volumes are float [B][K][H][W] (slice-major).  The 2D transform uses the in-place
-// Mallat layout (level l's LL band in the top-left H/2^l x W/2^l corner).  Passes:
-//   volume build (gather, with the cycle shift folded into the first row pass's reads),
-//   per level: analysis along x into a scratch volume, analysis along y back,
-//   one pass along z: Haar cascade + threshold + inverse cascade in registers (thread per pixel),
-//   per level (coarsest first): synthesis along y into scratch, synthesis along x back (the last
-//   one adds 1/H x the unshifted result into the accumulator U),
-//   TV weight per group (warp per group), aggregation (fp32 reductions) and the N x N box-sum
-//   divide.  Every pass is a streaming pass over the volume: HBM bound.
+// Layout: coefficient volumes are float [B][K][H][W] (slice-major); the 2D transform uses the
+// in-place Mallat layout (level l's LL band in the top-left H/2^l x W/2^l corner).  Per cycle
+// spin: one fused analysis launch per level (level 1 reads V straight from the image through
+// the match table, with the spin's circular shift; V is never stored), one pass along z (Haar
+// cascade + threshold + inverse cascade in registers, thread per pixel), one fused synthesis
+// launch per level (coarsest first; level 1 stores, then adds, 1/H x the unshifted result into
+// U).  Then one launch for the TV weights and the aggregation (fp32 reductions) and the N x N
+// box-sum divide.  The passes stream the volume (HBM) or are issue-bound.
 #include <cmath>
 #include <cstdint>
 
@@ -34,10 +33,7 @@ namespace {
 // (ana_step, syn_step) with the constants as instruction immediates.
 constexpr float kR2 = 0.70710678118654752f;
 
-__device__ __forceinline__ int wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
-
-// All passes use 3D grids (x tiles of 128 threads, rows, slices): no integer division by
-// runtime sizes in the streaming loops.
+// The z pass: 128-thread x tiles over (rows, images) grids.
 constexpr int TPB = 128;
 
 // ---- fused 2D passes: one level of analysis (x then y) or synthesis (y then x) per launch ----
