@@ -186,7 +186,7 @@ int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch, c
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
  * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,
- * and BLOCKS until the results are on the host.  The work is pipelined in up to 12 chunks
+ * and BLOCKS until the results are on the host.  The work is pipelined in up to 16 chunks
  * (images for B > 1; for B = 1 blocks of reference rows -- a 32-row first chunk, then equal
  * multiples of 16 -- whose pixel rows are copied in as bands): copies run on two
  * library-owned streams (created once per host thread and device) overlapped with the

@@ -366,7 +366,7 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
     // 16 so the tensor-core tiles of a chunk are the tiles of the whole call; a short first
     // chunk so the copies out start early)
 #ifndef GBM3D_HOST_NCH
-#define GBM3D_HOST_NCH 12
+#define GBM3D_HOST_NCH 16
 #endif
     const int units = B > 1 ? B : p.Ry;
     int ub[kMaxChunks + 1];
