@@ -40,3 +40,16 @@ def test_single_trial_is_one_call():
     torch.cuda.synchronize()
     # equal up to the order of the fp32 atomic reductions in the aggregation (run to run)
     np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), atol=1e-3, rtol=0)
+
+
+def test_batched_denoise_equals_single_images():
+    """A batch [B, H, W] runs every step batched (matching, stage 1, stage 2) and equals the
+    per-image calls (up to the order of the fp32 atomic reductions)."""
+    from paper_2103_10765_b200.denoise import denoise
+    imgs = [make_image(64, 96, 8, 2, 25.0, 10 + i) for i in range(3)]
+    z = torch.from_numpy(np.stack(imgs)).cuda()
+    yb = denoise(z, 25.0)
+    ys = [denoise(z[i].contiguous(), 25.0) for i in range(3)]
+    torch.cuda.synchronize()
+    for i in range(3):
+        np.testing.assert_allclose(yb[i].cpu().numpy(), ys[i].cpu().numpy(), atol=2e-3, rtol=0)
