@@ -371,10 +371,21 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             const int row = r + S * (m >> 3) + i, col = r + S * (m & 7);
             *reinterpret_cast<uint4*>(a_op + kmaj16_off(m, i)) = load16h(pl + row * PCH, col);
         }
+        tc::fence_proxy_async_smem();  // X and A (generic-proxy stores) -> the tensor core
+        tc::tc_fence_before();
         __syncthreads();
+        tc::tc_fence_after();
         if (threadIdx.x == 0) TC_TR(5, clock64());
-        // candidate norms N_q = vertical P-sums of hs (<= 64 M^2 < 2^24: exact in fp32)
-        for (int task = threadIdx.x; task < g.NT * 8; task += THREADS) {
+    }
+    const uint32_t tmem = *tslot;
+    if (threadIdx.x == 0) TC_TR(0, clock64());
+
+    if (warp != MMA_WARP) {
+        // candidate norms N_q = vertical P-sums of hs (<= 64 M^2 < 2^24: exact in fp32), only
+        // read by the epilogue: warps 0-7 make them while the MMA warp starts the first rows;
+        // a named barrier over those 256 threads closes the phase (hs lives in the staging
+        // area the epilogue overwrites afterwards)
+        for (int task = threadIdx.x; task < g.NT * 8; task += 32 * MMA_WARP) {
             const int t = task >> 3, k = task & 7;
             int o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -389,13 +400,8 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
             *reinterpret_cast<float4*>(nc + t * NB + 8 * k + 4) =
                 make_float4((float)o[4], (float)o[5], (float)o[6], (float)o[7]);
         }
-        tc::fence_proxy_async_smem();
-        tc::tc_fence_before();
-        __syncthreads();
-        tc::tc_fence_after();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * MMA_WARP) : "memory");
     }
-    const uint32_t tmem = *tslot;
-    if (threadIdx.x == 0) TC_TR(0, clock64());
 
     if (warp == MMA_WARP) {
         if (lane == 0) {

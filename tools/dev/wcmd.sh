@@ -1,6 +1,2 @@
-for i in 1 2; do
-GBM3D_LIB=paper_2103_10765_b200/libgbm3d.so python tools/dev/time_host.py c4
-GBM3D_LIB=variants/host16.so python tools/dev/time_host.py c4
-GBM3D_LIB=paper_2103_10765_b200/libgbm3d.so python tools/dev/time_host.py c3
-GBM3D_LIB=variants/host16.so python tools/dev/time_host.py c3
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
+for i in 1 2; do python tools/time_config.py --config c3 --reps 20; python tools/time_config.py --config c4 --reps 10; done
