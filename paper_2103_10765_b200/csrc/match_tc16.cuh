@@ -46,7 +46,10 @@ constexpr int MMAX = 362;        // exactness bound on max |z - c| (see header)
 #ifndef GBM3D_TC16_BULK_MIN
 #define GBM3D_TC16_BULK_MIN 16
 #endif
-constexpr int BULK_MIN = GBM3D_TC16_BULK_MIN;  // rows with this many passes (max over lanes) merge in bulk
+constexpr int BULK_MIN = GBM3D_TC16_BULK_MIN;
+#ifndef GBM3D_TC16_PREFETCH
+#define GBM3D_TC16_PREFETCH 1
+#endif  // rows with this many passes (max over lanes) merge in bulk
 }  // namespace tc16
 
 struct Tc16Geom {
@@ -235,6 +238,14 @@ __global__ void __launch_bounds__(tc16::THREADS, 1) match_tc16_kernel(MatchParam
     int* const hs = reinterpret_cast<int*>(sm + g.off_stg + 2 * g.PR * PCH * 2);
     const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
     {
+        // L2 prefetch of the rows a tile two tile-rows below needs (likely a CTA of a later
+        // wave): its first touch of HBM overlaps this tile's work instead of its own prologue
+        if (GBM3D_TC16_PREFETCH && threadIdx.x < 2 * g.PR) {
+            const int gy = gy0 + 2 * TY * S + (threadIdx.x >> 1);
+            const int gx = max(0, gx0) + 64 * (threadIdx.x & 1);
+            if (gy >= ylo && gy < yhi && gx < p.W)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(img + (int64_t)(gy - p.slab_y0) * p.W + gx));
+        }
         if (threadIdx.x == 0) {
             rng[0] = INT_MAX;
             rng[1] = INT_MIN;
