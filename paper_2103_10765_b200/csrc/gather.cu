@@ -40,13 +40,21 @@ __device__ __forceinline__ uint4 load8(const int16_t* __restrict__ base, int64_t
 }
 
 // groups, P = 8, tiled: CTA = a chunk of CH consecutive references of one grid row (CH x K
-// <= 2048 slots).  The bounding box of all the chunk's candidate blocks (a strip of the search
-// windows, e.g. 235 x 46 pixels for c3) is staged in shared memory with coalesced row loads,
+// <= 1024 slots).  The bounding box of all the chunk's candidate blocks (a strip of the search
+// windows, e.g. 139 x 46 pixels for c3) is staged in shared memory with coalesced row loads,
 // every slot's position is decoded once, then every 16-byte block row is assembled from shared
-// memory: HBM reads the image about once and the kernel is bound by the block writes.  A chunk
-// whose box does not fit (indices not from a local search) falls back to direct global loads.
-constexpr int SLOTS = 2048;             // slots (references x K) per CTA
-constexpr int BOX_WORDS = 11 * 1024;    // 44 KB staging: up to 22 K pixels
+// memory: HBM reads the image about once and the kernel is bound by the block writes.  The
+// staging buffer is small (20 KB: about 7 CTAs per SM); a chunk whose box does not fit is
+// redone in halves, down to single references whose blocks come from global memory (indices
+// not from a local search).
+#ifndef GBM3D_GATHER_SLOTS
+#define GBM3D_GATHER_SLOTS 1024
+#endif
+constexpr int SLOTS = GBM3D_GATHER_SLOTS;  // slots (references x K) per CTA
+#ifndef GBM3D_BOX_WORDS
+#define GBM3D_BOX_WORDS 5120
+#endif
+constexpr int BOX_WORDS = GBM3D_BOX_WORDS;  // staging words (2 pixels each)
 constexpr int GATHER_SMEM = (BOX_WORDS + SLOTS) * 4;
 __global__ void __launch_bounds__(256) gather_groups8_tiled_kernel(
         const int16_t* __restrict__ imgs, int H, int W, const int32_t* __restrict__ idx,
@@ -63,83 +71,102 @@ __global__ void __launch_bounds__(256) gather_groups8_tiled_kernel(
     const int32_t* __restrict__ tab = idx + ref0 * K;
     const int nslot = nref * K;
     const unsigned uW = (unsigned)W;
-    // decode every slot once; bounding box of the candidate top-lefts
-    int y0 = INT_MAX, y1 = -1, x0 = INT_MAX, x1 = -1;
+    // decode every slot once
     for (int q = threadIdx.x; q < nslot; q += blockDim.x) {
         const int c = __ldg(tab + q);
         const unsigned cy = (unsigned)c / uW, cx = (unsigned)c - cy * uW;
         const bool ok = c >= 0 && (int)cy <= H - 8 && (int)cx <= W - 8;
         pos[q] = ok ? (cy << 16 | cx) : ~0u;
-        if (ok) {
-            y0 = min(y0, (int)cy); y1 = max(y1, (int)cy);
-            x0 = min(x0, (int)cx); x1 = max(x1, (int)cx);
-        }
-    }
-    if (threadIdx.x == 0) { bb[0] = INT_MAX; bb[1] = -1; bb[2] = INT_MAX; bb[3] = -1; }
-    __syncthreads();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
-        y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
-        x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
-        x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&bb[0], y0); atomicMax(&bb[1], y1); atomicMin(&bb[2], x0); atomicMax(&bb[3], x1);
     }
     __syncthreads();
-    const int by0 = bb[0], bx0 = bb[2] & ~1;  // even column: 4-byte aligned staging words
-    const int rows = bb[1] - by0 + 8, cols = bb[3] + 8 - bx0;
-    const int pitch = ((cols + 9) & ~1) / 2;  // words per staged row (>= cols / 2 + 1)
-    const bool staged = bb[1] >= 0 && rows * pitch <= BOX_WORDS;
     const int16_t* __restrict__ img = imgs + (int64_t)b * H * W;
-    if (staged) {
-        // rows of the box as 32-bit words, coalesced per row: aligned word loads when W is even
-        // (bx0 is even, so every staged word starts on a 4-byte boundary), else element loads
-        if ((W & 1) == 0) {
-            const uint32_t* img32 = reinterpret_cast<const uint32_t*>(img);
-            const int W2 = W >> 1;
-            for (int u = threadIdx.x; u < rows * pitch; u += blockDim.x) {
-                const int r = u / pitch, cw = u - r * pitch;
-                const int gw = (bx0 >> 1) + cw;
-                box[u] = gw < W2 ? __ldg(img32 + (int64_t)(by0 + r) * W2 + gw) : 0u;
-            }
-        } else {
-            for (int u = threadIdx.x; u < rows * pitch; u += blockDim.x) {
-                const int r = u / pitch, cw = u - r * pitch;
-                const int gx = bx0 + 2 * cw;
-                const int16_t* src = img + (int64_t)(by0 + r) * W;
-                const uint32_t lo = gx < W ? (uint16_t)__ldg(src + gx) : 0u;
-                const uint32_t hi = gx + 1 < W ? (uint16_t)__ldg(src + gx + 1) : 0u;
-                box[u] = lo | (hi << 16);
+    uint4* const o = out + ref0 * K * 8;
+    // references [s0, s0 + sub) at a time: the whole chunk when its candidates' bounding box
+    // fits the staging buffer (the usual case), else halves of it, down to one reference
+    // whose blocks are then read straight from global memory
+    int sub = nref;
+    for (int s0 = 0; s0 < nref;) {
+        const int s1 = min(nref, s0 + sub);
+        int y0 = INT_MAX, y1 = -1, x0 = INT_MAX, x1 = -1;
+        for (int q = s0 * K + (int)threadIdx.x; q < s1 * K; q += blockDim.x) {
+            const uint32_t pq = pos[q];
+            if (pq != ~0u) {
+                const int cy = (int)(pq >> 16), cx = (int)(pq & 0xffffu);
+                y0 = min(y0, cy); y1 = max(y1, cy);
+                x0 = min(x0, cx); x1 = max(x1, cx);
             }
         }
-    }
-    __syncthreads();
-    // one item = one 8-pixel block row: (slot q of the chunk, row i); 32 lanes write 512 B
-    uint4* const o = out + ref0 * K * 8;
-    for (int it = threadIdx.x; it < nslot * 8; it += blockDim.x) {
-        const int q = it >> 3, i = it & 7;
-        const uint32_t pq = pos[q];
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (pq != ~0u) {
-            const int cy = (int)(pq >> 16), cx = (int)(pq & 0xffffu);
-            if (staged) {
-                const int e = cx - bx0;
-                const uint32_t* w = box + (cy - by0 + i) * pitch + (e >> 1);
-                const uint32_t a0 = w[0], a1 = w[1], a2 = w[2], a3 = w[3];
-                if ((e & 1) == 0) {
-                    v = make_uint4(a0, a1, a2, a3);
-                } else {
-                    const uint32_t a4 = w[4];
-                    v = make_uint4(__funnelshift_r(a0, a1, 16), __funnelshift_r(a1, a2, 16),
-                                   __funnelshift_r(a2, a3, 16), __funnelshift_r(a3, a4, 16));
+        if (threadIdx.x == 0) { bb[0] = INT_MAX; bb[1] = -1; bb[2] = INT_MAX; bb[3] = -1; }
+        __syncthreads();
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+            y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+            x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+            x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&bb[0], y0); atomicMax(&bb[1], y1); atomicMin(&bb[2], x0); atomicMax(&bb[3], x1);
+        }
+        __syncthreads();
+        const int by0 = bb[0], bx0 = bb[2] & ~1;  // even column: 4-byte aligned staging words
+        const int rows = bb[1] - by0 + 8, cols = bb[3] + 8 - bx0;
+        const int pitch = ((cols + 9) & ~1) / 2;  // words per staged row (>= cols / 2 + 1)
+        const bool staged = bb[1] >= 0 && rows * pitch <= BOX_WORDS;
+        if (!staged && bb[1] >= 0 && sub > 1) {  // retry these references in smaller groups
+            sub = (sub + 1) >> 1;
+            __syncthreads();
+            continue;
+        }
+        if (staged) {
+            // rows of the box as 32-bit words, coalesced per row: aligned word loads when W is
+            // even (bx0 is even, so every staged word starts on a 4-byte boundary)
+            if ((W & 1) == 0) {
+                const uint32_t* img32 = reinterpret_cast<const uint32_t*>(img);
+                const int W2 = W >> 1;
+                for (int u = threadIdx.x; u < rows * pitch; u += blockDim.x) {
+                    const int r = u / pitch, cw = u - r * pitch;
+                    const int gw = (bx0 >> 1) + cw;
+                    box[u] = gw < W2 ? __ldg(img32 + (int64_t)(by0 + r) * W2 + gw) : 0u;
                 }
             } else {
-                v = load8(imgs, ((int64_t)b * H + cy + i) * (int64_t)W + cx);
+                for (int u = threadIdx.x; u < rows * pitch; u += blockDim.x) {
+                    const int r = u / pitch, cw = u - r * pitch;
+                    const int gx = bx0 + 2 * cw;
+                    const int16_t* src = img + (int64_t)(by0 + r) * W;
+                    const uint32_t lo = gx < W ? (uint16_t)__ldg(src + gx) : 0u;
+                    const uint32_t hi = gx + 1 < W ? (uint16_t)__ldg(src + gx + 1) : 0u;
+                    box[u] = lo | (hi << 16);
+                }
             }
         }
-        o[it] = v;
+        __syncthreads();
+        // one item = one 8-pixel block row: (slot q, row i); 32 lanes write 512 B
+        for (int it = s0 * K * 8 + (int)threadIdx.x; it < s1 * K * 8; it += blockDim.x) {
+            const int q = it >> 3, i = it & 7;
+            const uint32_t pq = pos[q];
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (pq != ~0u) {
+                const int cy = (int)(pq >> 16), cx = (int)(pq & 0xffffu);
+                if (staged) {
+                    const int e = cx - bx0;
+                    const uint32_t* w = box + (cy - by0 + i) * pitch + (e >> 1);
+                    const uint32_t a0 = w[0], a1 = w[1], a2 = w[2], a3 = w[3];
+                    if ((e & 1) == 0) {
+                        v = make_uint4(a0, a1, a2, a3);
+                    } else {
+                        const uint32_t a4 = w[4];
+                        v = make_uint4(__funnelshift_r(a0, a1, 16), __funnelshift_r(a1, a2, 16),
+                                       __funnelshift_r(a2, a3, 16), __funnelshift_r(a3, a4, 16));
+                    }
+                } else {
+                    v = load8(imgs, ((int64_t)b * H + cy + i) * (int64_t)W + cx);
+                }
+            }
+            o[it] = v;
+        }
+        __syncthreads();  // the box is restaged by the next group
+        s0 = s1;
     }
 }
 

@@ -97,3 +97,31 @@ def test_invalid_index_gives_zero_block_and_errors():
     with pytest.raises(ValueError):
         g.gather_volume(torch.from_numpy(img[:60, :60].copy()).cuda(),
                         torch.from_numpy(idx).cuda(), 8)
+
+
+@pytest.mark.parametrize("H,W,s,r,K", [(256, 320, 3, 32, 32), (200, 256, 2, 32, 64), (160, 160, 1, 24, 16)])
+def test_groups_parity_wide_windows(H, W, s, r, K):
+    """Wide windows and dense grids: a chunk's candidate bounding box exceeds the staging
+    buffer, so the kernel retries the chunk's references in halves (down to one reference
+    with global loads); the groups must still be exact."""
+    g = _g()
+    img = config_images(CONFIGS["c3"])[0][:H, :W].copy()
+    idx, _, _ = oracle.block_match(img, 8, s, r, K, None)
+    got = g.gather_groups(torch.from_numpy(img).cuda(), torch.from_numpy(idx).cuda(), 8)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle.gather_groups(img, idx, 8))
+
+
+def test_groups_parity_global_indices():
+    """Indices from anywhere in the image (not a local search): the one-reference groups'
+    boxes still exceed the buffer and the blocks come straight from global memory."""
+    g = _g()
+    rng = np.random.default_rng(5)
+    img = rng.integers(-300, 300, (300, 280)).astype(np.int16)
+    Ry, Rx, K = 40, 37, 32
+    cy = rng.integers(0, 300 - 8 + 1, (Ry, Rx, K))
+    cx = rng.integers(0, 280 - 8 + 1, (Ry, Rx, K))
+    idx = (cy * 280 + cx).astype(np.int32)
+    got = g.gather_groups(torch.from_numpy(img).cuda(), torch.from_numpy(idx).cuda(), 8)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy(), oracle.gather_groups(img, idx, 8))

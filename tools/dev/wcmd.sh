@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
-for i in 1 2; do python tools/time_config.py --config c3 --reps 20; python tools/time_config.py --config c4 --reps 10; done
+for v in g_1024_5120 g_1024_4608 g_1024_4096 g_512_3072; do lib=variants/$v.so; echo $v; GBM3D_LIB=$lib python tools/dev/time_gather.py c3; GBM3D_LIB=$lib python tools/dev/time_gather.py c4; done
