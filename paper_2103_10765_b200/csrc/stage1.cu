@@ -47,6 +47,9 @@ constexpr int TPB = 128;
 constexpr int FT = 32;                 // coefficient tile (per subband)
 constexpr int FIN = 2 * FT + 9;        // 73 analysis inputs per axis
 constexpr int FTHREADS = 256;
+#ifndef GBM3D_S1_ANA_MINB
+#define GBM3D_S1_ANA_MINB 5  // 48 registers: 5 CTAs per SM (the shared-memory limit)
+#endif
 constexpr int SYN_IN = FT + FT + 4;    // 68: a[j0 .. j0+31] then d[j0-2 .. j0+33]
 
 __device__ __forceinline__ int mod_pos(int i, int n) {
@@ -83,7 +86,7 @@ __device__ __forceinline__ void syn_step(const float (&D)[5], float a, float& e,
 // slot k, the cycle spin's circular shift applied to (k, y, x) first; `src`
 // is then unused.  Otherwise `src` holds the band (the previous level's LL).
 template <bool GATHER>
-__global__ void __launch_bounds__(FTHREADS) s1_ana_xy_kernel(const float* __restrict__ src,
+__global__ void __launch_bounds__(FTHREADS, GBM3D_S1_ANA_MINB) s1_ana_xy_kernel(const float* __restrict__ src,
         int src_row0, const int16_t* __restrict__ img, const int32_t* __restrict__ idx, int N,
         float* __restrict__ ll_dst, int ll_row0, float* __restrict__ det, int K, int H,
         int W, int h, int w, int shift) {
