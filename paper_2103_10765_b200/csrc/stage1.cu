@@ -396,11 +396,12 @@ __global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __rest
     if (x >= w) return;
     constexpr int RPT = 2 * FT / (FTHREADS / 64);   // 16 rows per thread
     if (accumulate == 0) {
-        float* const o = dst + (int64_t)s * plane + (int64_t)dst_row0 * W + x;
+        float* o = dst + (int64_t)s * plane + (int64_t)(dst_row0 + y0 + (tid >> 6)) * W + x;
+        const int64_t rowstep = (int64_t)(FTHREADS / 64) * W;
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
+        for (int q = 0; q < RPT; ++q, o += rowstep) {
             const int r = (tid >> 6) + q * (FTHREADS / 64);
-            if (y0 + r < h) o[(int64_t)(y0 + r) * W] = out[r][c];
+            if (y0 + r < h) *o = out[r][c];
         }
     } else {
         // (S_-h R)[k][y][x] = R[k + h][y + h][x + h]: this element lands at (k-h, y-h, x-h)
@@ -411,12 +412,13 @@ __global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __rest
         const int kk = k >= shift ? k - shift : k - shift + K;
         const int xs = x >= shift ? x - shift : x - shift + W;
         float* const o = dst + (int64_t)(b * K + kk) * plane + xs;
-        // row y = y0 + (tid >> 6) + 4 q lands at y - shift (only y < shift wraps, to y - shift + H)
+        // row y = yb + 4 q lands at y - shift: one pointer step of 4 rows per q, except that
+        // y < shift (only q = 0 can have it: yb < shift <= 1) wraps to y - shift + H
         const int yb = y0 + (tid >> 6);
-        auto orow = [&](int q) {
-            const int y = yb + q * (FTHREADS / 64);
-            return o + (int64_t)(y >= shift ? y - shift : y - shift + H) * W;
-        };
+        const int64_t rowstep = (int64_t)(FTHREADS / 64) * W;
+        float* const pq0 = o + (int64_t)(yb >= shift ? yb - shift : yb - shift + H) * W;
+        float* const pq1 = o + (int64_t)(yb + FTHREADS / 64 - shift) * W;  // q >= 1, no wrap
+        auto orow = [&](int q) { return q == 0 ? pq0 : pq1 + (q - 1) * rowstep; };
         float old[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q)

@@ -1,2 +1,2 @@
-for i in 1 2; do for v in main ana5; do lib=variants/$v.so; [ $v = main ] && lib=paper_2103_10765_b200/libgbm3d.so; echo -n "$v "; GBM3D_LIB=$lib TAG=$v python tools/dev/time_stage1.py c3; done; done
-GBM3D_LIB=variants/ana5.so timeout 600 python -m pytest tests/test_gpu_stage1.py -q -x 2>&1 | tail -1
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:s1_syn_xy --launch-skip 2 -c 1 -o gpurun_out/s1_syn1 -f python tools/dev/stage1_once.py c3 > gpurun_out/ncu_s1c.log 2>&1; tail -1 gpurun_out/ncu_s1c.log
