@@ -50,6 +50,9 @@ constexpr int FTHREADS = 256;
 #ifndef GBM3D_S1_ANA_MINB
 #define GBM3D_S1_ANA_MINB 5  // 48 registers: 5 CTAs per SM (the shared-memory limit)
 #endif
+#ifndef GBM3D_S1_ANA_MINB_G
+#define GBM3D_S1_ANA_MINB_G 4  // the level-1 gather instance: 63 registers, no spills
+#endif
 constexpr int SYN_IN = FT + FT + 4;    // 68: a[j0 .. j0+31] then d[j0-2 .. j0+33]
 
 __device__ __forceinline__ int mod_pos(int i, int n) {
@@ -86,7 +89,7 @@ __device__ __forceinline__ void syn_step(const float (&D)[5], float a, float& e,
 // slot k, the cycle spin's circular shift applied to (k, y, x) first; `src`
 // is then unused.  Otherwise `src` holds the band (the previous level's LL).
 template <bool GATHER>
-__global__ void __launch_bounds__(FTHREADS, GBM3D_S1_ANA_MINB) s1_ana_xy_kernel(const float* __restrict__ src,
+__global__ void __launch_bounds__(FTHREADS, GATHER ? GBM3D_S1_ANA_MINB_G : GBM3D_S1_ANA_MINB) s1_ana_xy_kernel(const float* __restrict__ src,
         int src_row0, const int16_t* __restrict__ img, const int32_t* __restrict__ idx, int N,
         float* __restrict__ ll_dst, int ll_row0, float* __restrict__ det, int K, int H,
         int W, int h, int w, int shift) {
