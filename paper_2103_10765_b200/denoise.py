@@ -6,7 +6,8 @@ volume hard thresholding (``stage1_denoise``), stage-2 collaborative Wiener filt
 only for circular shifts, rounding and averaging of whole images (plumbing):
 
 * stage 1: Y_f = (1/H) sum_h S_-h phi(S_h Z) over the translation trials
-  h = 0, N/4, N/2 of the tiling reference grid (each trial matches its shifted image);
+  h = 0, N/4, N/2 of the tiling reference grid (each trial matches its shifted image; the
+  trials run as one batch through the matching and the thresholding);
 * stage 2: matching on the basic estimate (rounded to int16), Wiener
   filtering of the noisy image's groups with the basic estimate's spectra, aggregation.
 
@@ -23,18 +24,26 @@ from . import block_match, stage1_denoise, wiener_stage2
 
 def stage1(noisy, sigma, patch: int = 8, K: int = 16, radius: int = 16,
            trials: Optional[Sequence[int]] = None, levels: int = 3):
-    """Basic estimate (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA)."""
+    """Basic estimate (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA).  The
+    translation trials are stacked into one batch, so the matching and the global thresholding
+    each run as a single batched call over trials x images."""
     import torch
     trials = (0, patch // 4, patch // 2) if trials is None else tuple(trials)
     dims = (-2, -1)
+    x = noisy if noisy.dim() == 3 else noisy.unsqueeze(0)
+    B = x.shape[0]
+    z = torch.cat([torch.roll(x, shifts=(h, h), dims=dims) if h else x for h in trials]).contiguous()
+    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
+    sig = (sig.expand(B) if sig.numel() == 1 else sig).repeat(len(trials))
+    idx, dist, nv = block_match(z, patch, patch, radius, K, None, check=False)
+    y = stage1_denoise(z, idx, nv, patch, sig, levels)
     acc = None
-    for h in trials:
-        z = torch.roll(noisy, shifts=(h, h), dims=dims).contiguous() if h else noisy
-        idx, dist, nv = block_match(z, patch, patch, radius, K, None, check=False)
-        y = stage1_denoise(z, idx, nv, patch, sigma, levels)
-        y = torch.roll(y, shifts=(-h, -h), dims=dims) if h else y
-        acc = y if acc is None else acc + y
-    return acc / len(trials)
+    for t, h in enumerate(trials):
+        yt = y[t * B:(t + 1) * B]
+        yt = torch.roll(yt, shifts=(-h, -h), dims=dims) if h else yt
+        acc = yt if acc is None else acc + yt
+    out = acc / len(trials)
+    return out if noisy.dim() == 3 else out[0]
 
 
 def stage2(noisy, basic, sigma, patch: int = 8, stride: int = 3, K: int = 32, radius: int = 16):
