@@ -25,8 +25,9 @@
 //     (cp.async.bulk.tensor, zero fill outside the image) while the current tile is matched;
 //     range, centring, fp16 plane; X and A once the MMAs of the previous tile completed; the
 //     candidate norms once the epilogue left the previous tile;
-//   * MMA warp: one thread issues 4 MMAs (M128 N64 K16) per candidate row into one of NTS = 8
-//     TMEM stages (a ring that runs on across tiles);
+//   * MMA warp: one thread issues 4 MMAs (M128 N64 K16) per candidate row into one of NTS = 7
+//     TMEM stages (a ring that runs on across tiles); A (the tile's 128 reference patches) lives
+//     in tensor memory beside the stages, B in shared memory;
 //   * epilogue warp w (TMEM lane quarter w): accumulators -> u and a pass mask, staged in SMEM;
 //   * selector warp w: per-lane sorted top-(K-1) register lists (insertion network, one round
 //     per pass; bulk bitonic merges for dense rows), then the output rows straight from the
@@ -60,12 +61,26 @@ constexpr int TY = 16, TX = 8;
 constexpr int NB = 64;           // candidate columns per MMA tile (N)
 constexpr int PCH = 80;          // pixel box / fp16 plane width: 64 + 7 columns from a 16-byte
                                  // aligned start (TMA needs 16-byte aligned box coordinates)
-constexpr int NTS = 8;           // TMEM stages (64 columns each)
-constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, PRO_WARP0 = 9, NPRO = 4;
-constexpr int THREADS = 32 * (PRO_WARP0 + NPRO);
+constexpr int NTS = 7;           // TMEM stages (64 columns each)
+constexpr uint32_t TM_A = NTS * 64;  // TMEM column of the A operand (128 lanes x 32 columns)
+constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, PRO_WARP0 = 9, NPRO_MAX = 4;
+// Warp roles by list length.  K = 32 (KL = 31): epilogue (0-3), selectors (4-7), MMA (8),
+// producers (9-12, each writes the A rows of its lane quarter warp % 4 into TMEM); 13 warps.
+// K <= 16: the selector runs fast enough to wait on one epilogue warp per quarter, so each
+// quarter gets a second epilogue warp (12-15) and the two take its staged rows alternately;
+// 16 warps keep 128 registers per thread (4 per SMSP), so there are 3 producers (9-11) and
+// lane quarter 0's A rows go through a small shared buffer that the MMA warp copies in.  For
+// K = 32 the second epilogue warp costs the selector more issue slots than it saves (measured,
+// DESIGN.md).
+template <int KL>
+struct Tc16Cfg {
+    static constexpr int EH = KL <= 15 ? 2 : 1;          // epilogue warps per lane quarter
+    static constexpr int NPRO = EH == 2 ? 3 : 4;         // producer warps
+    static constexpr int EPI_WARP1 = PRO_WARP0 + NPRO;   // first warp of epilogue half 1
+    static constexpr int THREADS = 32 * (EPI_WARP1 + (EH == 2 ? EPI_WARPS : 0));
+};
 constexpr int NSLOT = 2;         // staged rows per lane quarter (epilogue one row ahead)
 constexpr int STG_PITCH = 68;    // words per lane and staged row: u[64], mask lo/hi, gate, row
-constexpr int A_BYTES = 128 * 128;
 constexpr int XP = (NB / 8) * 128;  // bytes per pre-shifted plane row (8 chunks of 8 x 16 B)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MMAX = 362;        // exactness bound on max |z - c| (see header)
@@ -81,24 +96,24 @@ constexpr int BULK_MIN = GBM3D_TC16_BULK_MIN;  // rows with this many passes (ma
 
 struct Tc16Geom {
     int NT, PR, NJ;
-    int off_a, off_x, off_nc, off_stg, off_pl, off_bar, total;
+    int off_x, off_nc, off_stg, off_pl, off_a0, off_bar, total;
     __host__ __device__ static Tc16Geom make(int S, int r) {
         using namespace tc16;
         Tc16Geom g;
         g.NT = 15 * S + 2 * r + 1;
         g.PR = g.NT + 7;
         g.NJ = 7 * S + 2 * r + 1;
-        g.off_a = 0;
-        g.off_x = A_BYTES;                 // pre-shifted plane
-        g.off_nc = g.off_x + g.PR * XP;    // candidate norms [NT][64] fp32
-        g.off_stg = g.off_nc + g.NT * NB * 4;
+        g.off_x = 0;                       // pre-shifted plane
+        g.off_nc = g.off_x + g.PR * XP;    // candidate norms [2][NT][64] fp32 (tile parity)
+        g.off_stg = g.off_nc + 2 * g.NT * NB * 4;
         g.off_pl = (g.off_stg + EPI_WARPS * NSLOT * 32 * STG_PITCH * 4 + 1023) & ~1023;  // TMA box
-        g.off_bar = (g.off_pl + g.PR * PCH * 2 + 15) & ~15;
-        // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT], raw, xa_ready, mma_done, nc_ready,
-        // epi_done, info_full/info_empty[NINFO]; gates[128], consumed[EPI_WARPS],
-        // info[NINFO][INFO_W], producer scratch[2*NPRO + 1], TMEM address
-        g.total = g.off_bar + (2 * NTS + 2 * EPI_WARPS * NSLOT + 5 + 2 * NINFO) * 8 +
-                  (EPI_WARPS * 32 + EPI_WARPS + NINFO * INFO_W + 2 * NPRO + 2) * 4 + 16;
+        g.off_a0 = (g.off_pl + g.PR * PCH * 2 + 15) & ~15;  // A rows of lane quarter 0 [32][32]
+        g.off_bar = g.off_a0 + 32 * 32 * 4;
+        // tfull/tempty[NTS], sfull/sempty[EPI_WARPS*NSLOT], raw, xa_ready, mma_done,
+        // nc_ready[2], epi_done[2], info_full/info_empty[NINFO]; gates[128], consumed[EPI_WARPS],
+        // info[NINFO][INFO_W], producer scratch[2*NPRO_MAX + 1], TMEM address
+        g.total = g.off_bar + (2 * NTS + 2 * EPI_WARPS * NSLOT + 7 + 2 * NINFO) * 8 +
+                  (EPI_WARPS * 32 + EPI_WARPS + NINFO * INFO_W + 2 * NPRO_MAX + 2) * 4 + 16;
         return g;
     }
 };
@@ -186,12 +201,6 @@ static __device__ __forceinline__ uint4 load16h(const __half* row, int c) {
                       __funnelshift_r(a2, a3, sh), __funnelshift_r(a3, a4, sh));
 }
 
-// Canonical K-major offset of (row, patch row i) for 128-byte K rows (64 fp16): core matrix
-// (row/8, i) at (row/8)*1024 + i*128, row-in-core * 16; patch row i = 8 fp16 = 16 bytes.
-static __device__ __forceinline__ int kmaj16_off(int row, int i) {
-    return (row >> 3) * 1024 + i * 128 + (row & 7) * 16;
-}
-
 // Candidate-row order of a tile.  Two "fill" rows first: f1 lies in the search window of every
 // reference of warps 0-2 and is outside warp 3's rows, f2 lies in every window of warp 3 and
 // outside warps 0-1's rows.  A warp's lists then all fill on the same row (one 39-round burst
@@ -268,10 +277,12 @@ struct Tc16Tile {
 };
 
 template <int S, int KL>
-__global__ void __launch_bounds__(tc16::THREADS, 1)
+__global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
     match_tc16_kernel(MatchParams p, const __grid_constant__ CUtensorMap tmap, int use_tma, int ntiles,
                       int sslot) {
     using namespace tc16;
+    constexpr int EPI_HALVES = Tc16Cfg<KL>::EH, NPRO = Tc16Cfg<KL>::NPRO;
+    constexpr int EPI_WARP1 = Tc16Cfg<KL>::EPI_WARP1;
     extern __shared__ __align__(1024) unsigned char sm[];
     const Tc16Geom g = Tc16Geom::make(S, p.r);
     constexpr int P = 8;
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
     const int kr1 = min(p.row_end, p.Ry_reg);
     const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
 
-    float* const nc = reinterpret_cast<float*>(sm + g.off_nc);
+    float* const nc2 = reinterpret_cast<float*>(sm + g.off_nc);  // nc of tile it: nc2 + (it & 1) NT NB
     __half* const pl = reinterpret_cast<__half*>(sm + g.off_pl);
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + g.off_bar);
     uint64_t* const tfull = bars;
@@ -291,21 +302,21 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
     uint64_t* const b_raw = sempty + EPI_WARPS * NSLOT;  // TMA box landed
     uint64_t* const b_xa = b_raw + 1;                    // X and A of the tile built
     uint64_t* const b_mma = b_raw + 2;                   // the tile's MMAs completed
-    uint64_t* const b_nc = b_raw + 3;                    // candidate norms built
-    uint64_t* const b_epi = b_raw + 4;                   // epilogue left the tile
-    uint64_t* const info_full = b_raw + 5;
+    uint64_t* const b_nc = b_raw + 3;                    // [2] candidate norms built (by tile parity)
+    uint64_t* const b_epi = b_raw + 5;                   // [2] epilogue left the tile (by tile parity)
+    uint64_t* const info_full = b_raw + 7;
     uint64_t* const info_empty = info_full + NINFO;
     volatile int* const gate_pub = reinterpret_cast<volatile int*>(info_empty + NINFO);
     volatile int* const consumed = gate_pub + EPI_WARPS * 32;  // rows taken by selector w (all tiles)
     volatile int* const info = consumed + EPI_WARPS;            // [NINFO][INFO_W]
     int* const red = const_cast<int*>(info + NINFO * INFO_W);
-    volatile int* const sched = red + 2 * NPRO;                 // tile fetched by the producers
+    volatile int* const sched = red + 2 * NPRO_MAX;             // tile fetched by the producers
     uint32_t* const tslot = reinterpret_cast<uint32_t*>(const_cast<int*>(sched + 1));
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NTS; ++i) {
             tc::mbar_init(&tfull[i], 1);
-            tc::mbar_init(&tempty[i], EPI_WARPS);
+            tc::mbar_init(&tempty[i], EPI_WARPS * EPI_HALVES);
         }
         for (int i = 0; i < EPI_WARPS * NSLOT; ++i) {
             tc::mbar_init(&sfull[i], 1);
@@ -314,11 +325,13 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
         tc::mbar_init(b_raw, 1);
         tc::mbar_init(b_xa, NPRO);
         tc::mbar_init(b_mma, 1);
-        tc::mbar_init(b_nc, NPRO);
-        tc::mbar_init(b_epi, EPI_WARPS);
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&b_nc[i], NPRO);
+            tc::mbar_init(&b_epi[i], EPI_WARPS * EPI_HALVES);
+        }
         for (int i = 0; i < NINFO; ++i) {
             tc::mbar_init(&info_full[i], 1);
-            tc::mbar_init(&info_empty[i], 1 + 2 * EPI_WARPS);
+            tc::mbar_init(&info_empty[i], 1 + (1 + EPI_HALVES) * EPI_WARPS);  // MMA, epilogue, selectors
         }
         tc::fence_mbar_init();
     }
@@ -329,7 +342,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
     tc::tc_fence_after();
     const uint32_t tmem = *tslot;
 
-    if (warp >= PRO_WARP0) {
+    if (warp >= PRO_WARP0 && warp < PRO_WARP0 + NPRO) {
         // ---------------- producers: the next tile's operands while the current one is matched
         const int tp = threadIdx.x - 32 * PRO_WARP0, pw = warp - PRO_WARP0;
         for (int it = 0;; ++it) {
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
             if (tile >= ntiles) {
                 if (tp == 0) {
                     const int slot = it % NINFO;
-                    if (it >= NINFO) tc::mbar_wait(&info_empty[slot], ((it / NINFO) - 1) & 1);
+                    if (it >= NINFO) tc::mbar_wait_long(&info_empty[slot], ((it / NINFO) - 1) & 1, 256);
                     info[slot * INFO_W] = -1;
                     tc::mbar_arrive(&info_full[slot]);
                 }
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
             const int cz = (lo + hi) >> 1;
             const bool skip = max(hi - cz, cz - lo) > MMAX;
             if (tp == 0) {
-                if (it >= NINFO) tc::mbar_wait(&info_empty[slot], ((it / NINFO) - 1) & 1);
+                if (it >= NINFO) tc::mbar_wait_long(&info_empty[slot], ((it / NINFO) - 1) & 1, 256);
                 volatile int* const in = info + slot * INFO_W;
                 in[0] = tile;
                 in[1] = T.bimg;
@@ -460,33 +473,14 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                 }
             }
             tc::named_bar(PRO_BAR, 32 * NPRO);
-            // (4) X and A, once the previous tile's MMAs no longer read them
-            if (tr) TC_TRP(2000 + it * 8 + 3, clock64());
-            if (it > 0) tc::mbar_wait(b_mma, (it - 1) & 1);
-            if (tr) TC_TRP(2000 + it * 8 + 4, clock64());
-            if (!skip) {
-                uint8_t* const xop = sm + g.off_x;
-                for (int u = tp; u < g.PR * NB; u += 32 * NPRO) {
-                    const int y = u >> 6, n = u & 63;
-                    *reinterpret_cast<uint4*>(xop + y * XP + n * 16) = load16h(pl + y * PCH, n + sh);
-                }
-                uint8_t* const a_op = sm + g.off_a;
-                for (int u = tp; u < 128 * P; u += 32 * NPRO) {
-                    const int i = u >> 7, m = u & 127;
-                    const int row = r + S * (m >> 3) + i, col = r + S * (m & 7);
-                    *reinterpret_cast<uint4*>(a_op + kmaj16_off(m, i)) = load16h(pl + row * PCH, col + sh);
-                }
-                tc::fence_proxy_async_smem();  // generic-proxy stores -> the tensor core
-            }
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(b_xa);
-            if (tr) TC_TRP(2000 + it * 8 + 5, clock64());
-            // (5) candidate norms N_q = P x P box sums of squares (integers < 2^24: exact in
-            // fp32), once the epilogue left the previous tile; a thread per (column, half)
-            if (it > 0) tc::mbar_wait(b_epi, (it - 1) & 1);
+            // (4) candidate norms N_q = P x P box sums of squares (integers < 2^24: exact in
+            // fp32) into the buffer of this tile's parity, free once the epilogue left tile it - 2
+            // (long ago: built during the previous tile); a thread per (column, half)
+            if (it > 1) tc::mbar_wait_long(&b_epi[it & 1], ((it >> 1) - 1) & 1, 512);
+            float* const nc = nc2 + (it & 1) * g.NT * NB;
             if (tr) TC_TRP(2000 + it * 8 + 6, clock64());
-            if (!skip) {
-                const int n = tp & 63, h = tp >> 6;
+            for (int task = tp; !skip && task < 2 * NB; task += 32 * NPRO) {
+                const int n = task & 63, h = task >> 6;
                 const int t0 = h ? (g.NT + 1) >> 1 : 0, t1 = h ? g.NT : (g.NT + 1) >> 1;
                 auto hsq = [&](int y) -> float {
                     const uint4 v = load16h(pl + y * PCH, n + sh);
@@ -524,15 +518,56 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(b_nc);
+            if (lane == 0) tc::mbar_arrive(&b_nc[it & 1]);
             if (tr) TC_TRP(2000 + it * 8 + 7, clock64());
+            // (5) X and A, once the previous tile's MMAs no longer read them
+            if (tr) TC_TRP(2000 + it * 8 + 3, clock64());
+            if (it > 0) tc::mbar_wait_long(b_mma, (it - 1) & 1, 256);
+            if (tr) TC_TRP(2000 + it * 8 + 4, clock64());
+            if (!skip) {
+                uint8_t* const xop = sm + g.off_x;
+                for (int u = tp; u < g.PR * NB; u += 32 * NPRO) {
+                    const int y = u >> 6, n = u & 63;
+                    *reinterpret_cast<uint4*>(xop + y * XP + n * 16) = load16h(pl + y * PCH, n + sh);
+                }
+                tc::fence_proxy_async_smem();  // generic-proxy stores -> the tensor core
+                // A: TMEM lane m = reference m = 8 a + b holds its patch, K = 8 i + j, two fp16
+                // per column; producer warp q writes its lane quarter (warp % 4)
+                const bool with_q0 = NPRO == 3 && (warp & 3) == 1;  // quarter 0 has no producer warp
+                for (int q = with_q0 ? 0 : (warp & 3); q <= (warp & 3); q += with_q0 ? 1 : 4) {
+                    const int m = 32 * q + lane;
+                    const int row = r + S * (m >> 3), col = r + S * (m & 7) + sh;
+                    uint32_t av[32];
+#pragma unroll
+                    for (int i = 0; i < P; ++i) {
+                        const uint4 v = load16h(pl + (row + i) * PCH, col);
+                        av[4 * i + 0] = v.x;
+                        av[4 * i + 1] = v.y;
+                        av[4 * i + 2] = v.z;
+                        av[4 * i + 3] = v.w;
+                    }
+                    if (with_q0 && q == 0) {  // copied into TMEM by the MMA warp (quarter 0)
+                        uint32_t* const a0 = reinterpret_cast<uint32_t*>(sm + g.off_a0);
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) a0[c * 32 + lane] = av[c];
+                    } else {
+                        tc::tmem_st32(tmem + TM_A + ((uint32_t)(32 * q) << 16), av);
+                        tc::tmem_wait_st();
+                    }
+                }
+                tc::tc_fence_before();
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(b_xa);
+            if (tr) TC_TRP(2000 + it * 8 + 5, clock64());
             tc::named_bar(PRO_BAR, 32 * NPRO);  // plane reads done before the next box lands
         }
     } else if (warp == MMA_WARP) {
-        // ---------------- MMA issuer: 4 x (M128 N64 K16) per candidate row
-        if (lane == 0) {
+        // ---------------- MMA issuer: 4 x (M128 N64 K16) per candidate row (lane 0; the whole
+        // warp when it also copies lane quarter 0's A rows into TMEM)
+        const unsigned wm = NPRO == 3 ? 0xffffffffu : 1u;
+        if (NPRO == 3 || lane == 0) {
             const uint32_t idesc = tc::idesc_f16f16_f32(128, NB);
-            const uint32_t aa = tc::smem_u32(sm + g.off_a);
             const uint32_t xa = tc::smem_u32(sm + g.off_x);
             int s = 0;
             for (int it = 0;; ++it) {
@@ -540,15 +575,28 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                 tc::mbar_wait(&info_full[slot], (it / NINFO) & 1);
                 const volatile int* const in = info + slot * INFO_W;
                 const int tile = in[0], ky0 = in[2], step = in[4], skip = in[5];
-                tc::mbar_arrive(&info_empty[slot]);
+                __syncwarp(wm);
+                if (lane == 0) tc::mbar_arrive(&info_empty[slot]);
                 if (tile < 0) break;
                 tc::mbar_wait(b_xa, it & 1);
-                if (it < 40) TC_TRP(3000 + it * 4, clock64());
-                tc::tc_fence_after();
+                if (lane == 0 && it < 40) TC_TRP(3000 + it * 4, clock64());
                 if (skip) {
-                    tc::mbar_arrive(b_mma);
+                    __syncwarp(wm);
+                    if (lane == 0) tc::mbar_arrive(b_mma);
                     continue;
                 }
+                if (NPRO == 3) {  // A rows of lane quarter 0: shared buffer -> TMEM (this warp's quarter)
+                    const uint32_t* const a0 = reinterpret_cast<const uint32_t*>(sm + g.off_a0);
+                    uint32_t av[32];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) av[c] = a0[c * 32 + lane];
+                    tc::tmem_st32(tmem + TM_A, av);
+                    tc::tmem_wait_st();
+                    tc::tc_fence_before();
+                    __syncwarp(wm);
+                }
+                tc::tc_fence_after();
+                if (lane == 0) {
                 const int gy0 = S * ky0 - r;
                 const int t_lo = max(0, -gy0), t_hi = min(g.NT - 1, (p.H - P) - gy0);
                 RowSeq seq;
@@ -562,18 +610,19 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                     const uint32_t bb = xa + (uint32_t)(t * XP);
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_f16(tmem + (uint32_t)(ts * NB), tc::smem_desc(aa + ks * 256, 128, 1024),
-                                    tc::smem_desc(bb + ks * 2 * XP, XP, 128), idesc, ks);
+                        tc::mma_f16_ts(tmem + (uint32_t)(ts * NB), tmem + TM_A + ks * 8,
+                                       tc::smem_desc(bb + ks * 2 * XP, XP, 128), idesc, ks);
                     tc::mma_commit(&tfull[ts]);
                 }
                 tc::mma_commit(b_mma);  // X and A free once these MMAs completed
                 if (it < 40) TC_TRP(3000 + it * 4 + 1, clock64());
+                }
+                __syncwarp(wm);  // the warp stays converged for the next tile's TMEM copy
             }
         }
-        __syncwarp();
-    } else if (warp < EPI_WARPS) {
+    } else if (warp < EPI_WARPS || (EPI_HALVES == 2 && warp >= EPI_WARP1)) {
         // ---------------- epilogue warp w: accumulators of lane quarter w -> staged rows
-        const int w = warp;
+        const int w = warp & 3, half = warp >= EPI_WARP1 ? 1 : 0;
         const int a = 4 * w + (lane >> 3), bb = lane & 7;
         const uint32_t taddr = tmem + ((uint32_t)(32 * w) << 16);
         const int gate0 = p.tdr0 + 1;
@@ -602,7 +651,8 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                                            : 0ull;
             RowSeq seq;
             seq.init(S, r, t_lo, t_hi, step);
-            tc::mbar_wait(b_nc, it & 1);
+            tc::mbar_wait(&b_nc[it & 1], (it >> 1) & 1);
+            const float* const nc = nc2 + (it & 1) * g.NT * NB;
             if (lane == 0 && it < 40) TC_TRP(4000 + it * 16 + w * 4, clock64());
             if (!skip) {
                 const float Nr = nc[ty * NB + tx];
@@ -612,32 +662,32 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                 for (int k = 0; k < nseq; ++k, ++s) {
                     const int ts = s % NTS;
                     const int t = seq.next();
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6400 + (used - tile_start), clock64());
                     tc::mbar_wait(&tfull[ts], (s / NTS) & 1);
                     if (!(warp_active && t >= wt0 && t <= wt1)) {
                         __syncwarp();
                         if (lane == 0) tc::mbar_arrive(&tempty[ts]);
                         continue;
                     }
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6500 + (used - tile_start), clock64());
                     const int slot = used % NSLOT;
-                    if (lane == 0 && it < 40 && used == tile_start) TC_TRP(4000 + it * 16 + w * 4 + 3, clock64());
+                    static_assert(NSLOT == 2, "half h stages the rows of slot h");
+                    if (EPI_HALVES == 2 && slot != half) {  // the other half stages this row
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                        ++used;
+                        continue;
+                    }
                     if (used >= NSLOT) tc::mbar_wait(&sempty[w * NSLOT + slot], ((used / NSLOT) - 1) & 1);
-                    if (lane == 0 && it < 40 && used == tile_start) TC_TRP(4700 + it * 8 + w, clock64());
-                    // the tile's first row passes its whole window (gate0); later rows take the
-                    // gates the selector published for this tile (it has taken the first row),
-                    // and while some list is filling, the gates of every row staged so far
                     int gate = gate0;
                     if (used > tile_start) {
-                        while (consumed[w] <= tile_start) {
-                        }
+                        while (consumed[w] <= tile_start) __nanosleep(32);
                         gate = gate_pub[w * 32 + lane];
                         if (__any_sync(0xffffffffu, gate == gate0 && refok)) {
-                            while (consumed[w] < used) {
-                            }
+                            while (consumed[w] < used) __nanosleep(32);
                             gate = gate_pub[w * 32 + lane];
                         }
                     }
-                    // u = N_q - 2 <f_p, f_q> passes iff u < T = gate - N_p; stage v = u - T
-                    // (exact for every passing candidate, sign-correct for the rest): d = v + gate
                     const float Tg = (float)(gate - __float2int_rn(Nr));
                     uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                     tc::tc_fence_after();
@@ -662,7 +712,6 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                             v[4 * q + 2] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 2]), -2.f, n4.z - Tg);
                             v[4 * q + 3] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 3]), -2.f, n4.w - Tg);
                         }
-                        // shift the sign bits in, highest column first: bit j of msk = column j passes
                         uint32_t& m = msk[ch >> 1];
 #pragma unroll
                         for (int j = 15; j >= 0; --j) m = __funnelshift_l(__float_as_uint(v[j]), m, 1);
@@ -674,7 +723,6 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                     tc::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&tempty[ts]);
-
                     const bool rowin = refok && t >= S * a && t <= S * a + 2 * r;
                     uint64_t mm = rowin ? ((((uint64_t)msk[1]) << 32 | msk[0]) & cm) : 0ull;
                     if (t == ty) mm &= ~(1ull << tx);  // the reference itself is slot 0
@@ -682,15 +730,16 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
                         make_uint4((uint32_t)mm, (uint32_t)(mm >> 32), (uint32_t)gate, (uint32_t)t);
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&sfull[w * NSLOT + slot]);
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6700 + (used - tile_start), clock64());
                     if (lane == 0 && it < 40 && used == tile_start) TC_TRP(4000 + it * 16 + w * 4 + 1, clock64());
                     ++used;
                 }
             }
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(b_epi);  // nc no longer read for this tile
+            if (lane == 0) tc::mbar_arrive(&b_epi[it & 1]);  // nc buffer (it & 1) free again
             if (lane == 0 && it < 40) TC_TRP(4000 + it * 16 + w * 4 + 2, clock64());
         }
-    } else {
+    } else if (warp >= SEL_WARP0 && warp < SEL_WARP0 + EPI_WARPS) {
         // ---------------- selector warp w: per-lane top-(K-1) lists, then the output rows
         const int w = warp - SEL_WARP0;
         const int a = 4 * w + (lane >> 3), bb = lane & 7;
@@ -729,7 +778,9 @@ __global__ void __launch_bounds__(tc16::THREADS, 1)
             }
             for (int k = 0; k < nrel; ++k, ++used) {
                 const int slot = used % NSLOT;
+                if (lane == 0 && it == 5 && w == 0) TC_TRP(6200 + k, clock64());
                 tc::mbar_wait(&sfull[w * NSLOT + slot], (used / NSLOT) & 1);
+                if (lane == 0 && it == 5 && w == 0) TC_TRP(6300 + k, clock64());
                 const uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                 const uint4 hdr = *reinterpret_cast<const uint4*>(stg + 64);
                 uint32_t mlo = hdr.x, mhi = hdr.y;
@@ -947,7 +998,7 @@ cudaError_t launch_tc16(const MatchParams& p, cudaStream_t stream, int* launches
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
     static std::atomic<unsigned> calls{0};
     const int sslot = (int)(calls.fetch_add(1u) % tc16::NSCHED);
-    kern<<<grid, tc16::THREADS, g.total, stream>>>(p, tm, use_tma, (int)ntiles, sslot);
+    kern<<<grid, tc16::Tc16Cfg<KL>::THREADS, g.total, stream>>>(p, tm, use_tma, (int)ntiles, sslot);
     if (launches) ++*launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

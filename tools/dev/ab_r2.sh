@@ -6,4 +6,4 @@ for lib in paper_2103_10765_b200/libgbm3d.so variants/libgbm3d_r1.so; do
     GBM3D_LIB=$lib timeout 120 python tools/time_config.py --config $c --reps 10 2>&1 | tail -1 | sed "s|^|$lib |"
   done
 done
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -5
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -5

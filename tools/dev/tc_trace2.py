@@ -23,5 +23,8 @@ for it in range(12):
     ep = [rel(t[4000 + it * 16 + k]) for k in (0, 1, 2)] + ["init", rel(t[4400 + it * 8]), "tfull", rel(t[4000 + it * 16 + 3]), "sempty", rel(t[4700 + it * 8])]
     se = [[rel(t[5000 + it * 16 + w * 4 + k]) for k in range(4)] for w in range(4)]
     print(it, pr, mm, ep, se)
-print("tile 5 selector w0 rows (end time, R):")
-print([(rel(t[6000 + k]), int(t[6100 + k])) for k in range(48)])
+print("tile 5 w0 per row: sel wait-start, sfull got, end, R | epi: start, tfull got, sempty got, staged")
+for k in range(48):
+    print(k, rel(t[6200 + k]), rel(t[6300 + k]), rel(t[6000 + k]), int(t[6100 + k]), "|",
+          rel(t[6400 + k]), rel(t[6500 + k]), rel(t[6600 + k]), "gate", rel(t[6800 + k]), "ld", rel(t[6900 + k]),
+          "cmp", rel(t[7000 + k]), rel(t[6700 + k]))
