@@ -6,7 +6,8 @@ PAPER.md:132-149 (section "Global Volume Hard Thresholding") and :154-206 (forma
   U_h    = S_-h T3D^-1( Upsilon( T3D( S_h V ) ) ),
   U      = (1/H) sum_h U_h, H = 2, h = 0, 1,
   w_pq   = 1 / TV(U_pq)                                  (PAPER.md:194-197),
-  Y(x)   = sum w_pq U_pq^x(x) / sum w_pq chi_x(x)        (PAPER.md:190; pads left out, :142).
+  Y(x)   = sum w_pq U_pq^x(x) / sum w_pq chi_x(x)        (PAPER.md:190; pads left out, :142),
+  Y_f    = (1/H) sum_h S_-h phi(S_h Z)                   (translation trials).
 Parameters: 2D biorthogonal 1.5 wavelets in space, Haar along the group,
 3 levels, hard thresholds lambda_l = sigma (3.6 - 0.3 l).  Readings S1-S7 in DESIGN.md.
 
@@ -111,21 +112,30 @@ def spatial_level_map(H: int, W: int, levels: int) -> np.ndarray:
     return lev
 
 
-def w3d_threshold(V: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
-    """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2).  `lam_scale`
-    (tests only) scales the thresholds, to find the decisions that sit within rounding of them."""
-    K, H, W = V.shape
+def upsilon(T: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
+    """Upsilon on a coefficient volume T [K, H, W] in the in-place layout: keep |alpha| >= lambda
+     with lambda_l = sigma (3.6 - 0.3 l) for the spatial level l of the
+    coefficient (the final LL band counts as level L); the coefficients that are
+    approximations both in space (LL_L) and along z are always kept (reading S2)."""
+    K, H, W = T.shape
     lz = min(levels, int(math.log2(K)))
-    T = haar_z(dwt2(V, levels), lz)
     lev = spatial_level_map(H, W, levels)
     lam = lam_scale * sigma * (3.6 - 0.3 * lev)         # PAPER.md:241
     keep = np.abs(T) >= lam[None]                        # Upsilon, PAPER.md:173-178
-    # the coefficients that are approximations in space (LL_L) and along z are kept (S2)
     hL, wL = H >> levels, W >> levels
     zapprox = np.zeros(K, dtype=bool)
     zapprox[:: 1 << lz] = True
     keep[np.ix_(zapprox, np.arange(hL), np.arange(wL))] = True
-    return idwt2(haar_z(np.where(keep, T, 0.0), lz, inverse=True), levels)
+    return np.where(keep, T, 0.0)
+
+
+def w3d_threshold(V: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
+    """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2).  `lam_scale`
+    (tests only) scales the thresholds, to find the decisions that sit within rounding of them."""
+    K = V.shape[0]
+    lz = min(levels, int(math.log2(K)))
+    T = haar_z(dwt2(V, levels), lz)
+    return idwt2(haar_z(upsilon(T, sigma, levels, lam_scale), lz, inverse=True), levels)
 
 
 def threshold_margin(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)) -> float:
@@ -185,3 +195,16 @@ def stage1(noisy: np.ndarray, idx: np.ndarray, n_valid: np.ndarray, patch: int, 
                 num[cy:cy + N, cx:cx + N] += w * G[k]
                 den[cy:cy + N, cx:cx + N] += w
     return num / den
+
+
+def translation_trials(noisy: np.ndarray, sigma: float, patch: int, K: int, radius: int,
+                       trials=(0, 2, 4), levels: int = 3, shifts=(0, 1)) -> np.ndarray:
+    """Y_f = (1/H) sum_h S_-h( phi(S_h Z) ) (Eq. (10)): phi = block matching
+    of the shifted image on the tiling grid (stride = N, PAPER.md:156-158) followed by stage1;
+    S_h = circular shift of the image by h pixels along both axes (reading S8)."""
+    acc = np.zeros(noisy.shape)
+    for h in trials:
+        Zh = np.roll(noisy, (h, h), axis=(0, 1))
+        idx, _dist, nv = oracle.block_match(Zh, patch, patch, radius, K, None)
+        acc += np.roll(stage1(Zh, idx, nv, patch, sigma, levels, shifts), (-h, -h), axis=(0, 1))
+    return acc / len(trials)
