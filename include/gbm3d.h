@@ -175,13 +175,31 @@ int gbm3d_wiener_stage2(const int16_t* noisy, const float* basic, int B, int H, 
  * workspace: gbm3d_stage1_workspace_bytes(B, H, W, patch, K) bytes (3 float volumes + 2 planes).
  * fp32 with atomic accumulation: matches a float64 evaluation within DESIGN.md's tolerance.
  * The translation trials of PAPER.md:203 (match and filter circularly shifted images, shift
- * back, average) are the caller's: each trial is a gbm3d_block_match + gbm3d_stage1_denoise.
+ * back, average) compose gbm3d_shift_trials, one batched gbm3d_block_match + this call over
+ * the T x B shifted images, and gbm3d_unshift_mean.
  * Errors: GBM3D_ERR_ARG (null pointers, sizes, small workspace), GBM3D_ERR_UNSUPPORTED (K not a
  * power of two or > 32, patch > 16, levels > 5), GBM3D_ERR_CUDA. */
 size_t gbm3d_stage1_workspace_bytes(int B, int H, int W, int patch, int K);
 int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch, const int32_t* idx,
                          const int32_t* n_valid, int K, const float* sigmas, int levels, float* out,
                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- Translation trials of stage 1 (Eq. (10)):
+ *   Y_f = (1/T) sum_t S_-h_t( phi(S_h_t Z) ),  S_h = circular shift by h pixels along both
+ * image axes (reading S8).  shifts: HOST int array of T trial offsets, each in
+ * [0, min(H, W)), 1 <= T <= GBM3D_MAX_TRIALS (the paper uses h = 0, N/4, N/2).
+ * gbm3d_shift_trials: imgs device int16 [B][H][W] -> out device int16 [T][B][H][W] with
+ *   out[t][b][y][x] = imgs[b][(y - h_t) mod H][(x - h_t) mod W]   (a batch for the matcher);
+ * gbm3d_unshift_mean: ys device float32 [T][B][H][W] (phi of each shifted image) -> out device
+ *   float32 [B][H][W], out[b][y][x] = (1/T) sum_t ys[t][b][(y + h_t) mod H][(x + h_t) mod W].
+ * Both enqueue on `stream` and allocate nothing; exact copies / an fp32 mean of T terms.
+ * Errors: GBM3D_ERR_ARG (null pointers, sizes, T or a shift out of range, T*B > 65535),
+ * GBM3D_ERR_UNSUPPORTED (H > 65535), GBM3D_ERR_CUDA. */
+#define GBM3D_MAX_TRIALS 16
+int gbm3d_shift_trials(const int16_t* imgs, int B, int H, int W, const int* shifts, int T,
+                       int16_t* out, void* stream);
+int gbm3d_unshift_mean(const float* ys, int T, int B, int H, int W, const int* shifts,
+                       float* out, void* stream);
 
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device

@@ -15,7 +15,7 @@ __all__ = [
     "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
     "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
     "last_launch_count", "version", "gather_groups", "gather_volume", "wiener_stage2",
-    "stage1_denoise",
+    "stage1_denoise", "shift_trials", "unshift_mean",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -69,6 +69,8 @@ def load_library():
                                        ctypes.c_size_t, vp]),
         "gbm3d_wiener_stage2": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp,
                                       vp, ctypes.c_size_t, vp]),
+        "gbm3d_shift_trials": (i32, [vp, i32, i32, i32, vp, i32, vp, vp]),
+        "gbm3d_unshift_mean": (i32, [vp, i32, i32, i32, i32, vp, vp, vp]),
         "gbm3d_last_launch_count": (i32, []),
         "gbm3d_strerror": (ctypes.c_char_p, [i32]),
         "gbm3d_version": (ctypes.c_char_p, []),
@@ -114,6 +116,13 @@ def _stream_handle(device):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def _on(device):
+    """The library launches on the current device: make the tensors' device current for the
+    call (a tensor on another GPU than the current one would otherwise fail to launch)."""
+    import torch
+    return torch.cuda.device(device)
+
+
 def _check_cuda_int16(t, name):
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int16:
@@ -126,8 +135,9 @@ def check_range(img, patch: int) -> bool:
     """P^2 (max-min)^2 <= 2^31-1 on the device (reading R10).  Synchronises the stream."""
     _check_cuda_int16(img, "img")
     ok = ctypes.c_int(0)
-    st = load_library().gbm3d_check_range(ctypes.c_void_p(img.data_ptr()), img.numel(), patch,
-                                          ctypes.byref(ok), _stream_handle(img.device))
+    with _on(img.device):
+        st = load_library().gbm3d_check_range(ctypes.c_void_p(img.data_ptr()), img.numel(), patch,
+                                              ctypes.byref(ok), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "check_range")
     return bool(ok.value)
@@ -169,10 +179,11 @@ def block_match(img, patch: int, stride: int, radius: int, K: int, tau: Optional
     Ry, Rx = grid_dims(H, W, patch, stride)
     shape = ((B,) if batched else ()) + (Ry, Rx, K)
     idx, dist, nv = _alloc_out(shape, img.device, out)
-    st = load_library().gbm3d_block_match_ex(
-        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
-        METHODS[method], ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
-        ctypes.c_void_p(nv.data_ptr() if nv is not None else 0), _stream_handle(img.device))
+    with _on(img.device):
+        st = load_library().gbm3d_block_match_ex(
+            ctypes.c_void_p(img.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
+            METHODS[method], ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+            ctypes.c_void_p(nv.data_ptr() if nv is not None else 0), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "block_match")
     return idx, dist, nv
@@ -188,11 +199,12 @@ def block_match_rows(slab, slab_y0: int, H: int, W: int, patch: int, stride: int
         raise ValueError("slab must be [rows, W]")
     _, Rx = grid_dims(H, W, patch, stride)
     idx, dist, nv = _alloc_out((row_end - row_begin, Rx, K), slab.device, out)
-    st = load_library().gbm3d_block_match_rows(
-        ctypes.c_void_p(slab.data_ptr()), slab_y0, slab.shape[0], H, W, patch, stride, radius, K,
-        _tau(tau), row_begin, row_end, ctypes.c_void_p(idx.data_ptr()),
-        ctypes.c_void_p(dist.data_ptr()), ctypes.c_void_p(nv.data_ptr() if nv is not None else 0),
-        _stream_handle(slab.device))
+    with _on(slab.device):
+        st = load_library().gbm3d_block_match_rows(
+            ctypes.c_void_p(slab.data_ptr()), slab_y0, slab.shape[0], H, W, patch, stride, radius,
+            K, _tau(tau), row_begin, row_end, ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(dist.data_ptr()),
+            ctypes.c_void_p(nv.data_ptr() if nv is not None else 0), _stream_handle(slab.device))
     if st != 0:
         raise GBM3DError(st, "block_match_rows")
     return idx, dist, nv
@@ -213,20 +225,32 @@ def block_match_host(h_img, patch: int, stride: int, radius: int, K: int,
     B, H, W = x.shape
     Ry, Rx = grid_dims(H, W, patch, stride)
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    device = torch.device(device)
     need = host_workspace_bytes(B, H, W, patch, stride, K)
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=device)
+    elif not workspace.is_cuda or workspace.device != device or not workspace.is_contiguous() \
+            or workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"workspace must be a contiguous buffer of >= {need} bytes on {device}")
     if out is None:
         pin = torch.cuda.is_available()
         out = (torch.empty((B, Ry, Rx, K), dtype=torch.int32, pin_memory=pin),
                torch.empty((B, Ry, Rx, K), dtype=torch.int32, pin_memory=pin),
                torch.empty((B, Ry, Rx), dtype=torch.int32, pin_memory=pin))
+    else:
+        # the library copies B Ry Rx K int32 into each host buffer: check before it does
+        for t, shp, n in ((out[0], (B, Ry, Rx, K), "idx"), (out[1], (B, Ry, Rx, K), "dist"),
+                          (out[2], (B, Ry, Rx), "n_valid")):
+            if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != torch.int32 \
+                    or tuple(t.shape) != shp or not t.is_contiguous():
+                raise ValueError(f"out {n} must be a contiguous CPU int32 tensor {shp}")
     idx, dist, nv = out
-    st = load_library().gbm3d_block_match_host(
-        ctypes.c_void_p(x.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
-        ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
-        ctypes.c_void_p(nv.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
-        _stream_handle(device))
+    with _on(device):
+        st = load_library().gbm3d_block_match_host(
+            ctypes.c_void_p(x.data_ptr()), B, H, W, patch, stride, radius, K, _tau(tau),
+            ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+            ctypes.c_void_p(nv.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+            workspace.numel() * workspace.element_size(), _stream_handle(device))
     if st != 0:
         raise GBM3DError(st, "block_match_host")
     return out
@@ -258,9 +282,10 @@ def gather_groups(img, idx, patch: int, out=None):
         out = torch.empty(shape, dtype=torch.int16, device=img.device)
     elif out.dtype != torch.int16 or tuple(out.shape) != shape or not out.is_contiguous():
         raise ValueError(f"out must be contiguous int16 {shape}")
-    st = load_library().gbm3d_gather_groups(
-        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), Ry,
-        Rx, K, ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
+    with _on(img.device):
+        st = load_library().gbm3d_gather_groups(
+            ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), Ry,
+            Rx, K, ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "gather_groups")
     return out
@@ -284,12 +309,45 @@ def gather_volume(img, idx, patch: int, out=None):
         out = torch.empty(shape, dtype=torch.int16, device=img.device)
     elif out.dtype != torch.int16 or tuple(out.shape) != shape or not out.is_contiguous():
         raise ValueError(f"out must be contiguous int16 {shape}")
-    st = load_library().gbm3d_gather_volume(
-        ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), K,
-        ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
+    with _on(img.device):
+        st = load_library().gbm3d_gather_volume(
+            ctypes.c_void_p(img.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()), K,
+            ctypes.c_void_p(out.data_ptr()), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "gather_volume")
     return out
+
+
+def _sigmas(sigma, B: int, device):
+    """One float32 noise level per image on `device` (a scalar is broadcast): the kernels read
+    sigmas[b] for every b < B, so the length is checked here (the C ABI cannot)."""
+    import torch
+    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
+    if sig.numel() == 1:
+        sig = sig.expand(B)
+    if sig.numel() != B:
+        raise ValueError(f"sigma must be a scalar or have one entry per image ({B})")
+    return sig.contiguous().to(device)
+
+
+def _float_out(out, like):
+    import torch
+    if out is None:
+        return torch.empty(like.shape, dtype=torch.float32, device=like.device)
+    if out.dtype != torch.float32 or out.shape != like.shape or not out.is_contiguous() \
+            or out.device != like.device:
+        raise ValueError(f"out must be a contiguous float32 tensor {tuple(like.shape)} on {like.device}")
+    return out
+
+
+def _workspace(ws, need: int, device):
+    import torch
+    if ws is None:
+        return torch.empty(need, dtype=torch.uint8, device=device)
+    if not ws.is_cuda or ws.device != device or not ws.is_contiguous() \
+            or ws.numel() * ws.element_size() < need:
+        raise ValueError(f"workspace must be a contiguous buffer of >= {need} bytes on {device}")
+    return ws
 
 
 def wiener_stage2(noisy, basic, idx, n_valid, patch: int, sigma, out=None, workspace=None):
@@ -306,21 +364,23 @@ def wiener_stage2(noisy, basic, idx, n_valid, patch: int, sigma, out=None, works
     batched = noisy.dim() == 3
     B = noisy.shape[0] if batched else 1
     H, W = noisy.shape[-2], noisy.shape[-1]
+    if idx.dim() != (4 if batched else 3) or (batched and idx.shape[0] != B):
+        raise ValueError("idx must be [(B,) Ry, Rx, K] matching noisy")
     Ry, Rx, K = idx.shape[-3], idx.shape[-2], idx.shape[-1]
-    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
-    if sig.numel() == 1:
-        sig = sig.expand(B)
-    sig = sig.contiguous().to(noisy.device)
-    if out is None:
-        out = torch.empty(noisy.shape, dtype=torch.float32, device=noisy.device)
+    if Ry > H - patch + 1 or Rx > W - patch + 1:
+        raise ValueError("idx grid larger than the image's reference grid")
+    if tuple(n_valid.shape) != tuple(idx.shape[:-1]):
+        raise ValueError("n_valid must be idx.shape[:-1]")
+    sig = _sigmas(sigma, B, noisy.device)
+    out = _float_out(out, noisy)
     need = int(load_library().gbm3d_wiener_workspace_bytes(B, H, W))
-    if workspace is None:
-        workspace = torch.empty(need, dtype=torch.uint8, device=noisy.device)
-    st = load_library().gbm3d_wiener_stage2(
-        ctypes.c_void_p(noisy.data_ptr()), ctypes.c_void_p(basic.data_ptr()), B, H, W, patch,
-        ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(n_valid.data_ptr()), Ry, Rx, K,
-        ctypes.c_void_p(sig.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_handle(noisy.device))
+    workspace = _workspace(workspace, need, noisy.device)
+    with _on(noisy.device):
+        st = load_library().gbm3d_wiener_stage2(
+            ctypes.c_void_p(noisy.data_ptr()), ctypes.c_void_p(basic.data_ptr()), B, H, W, patch,
+            ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(n_valid.data_ptr()), Ry, Rx, K,
+            ctypes.c_void_p(sig.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(workspace.data_ptr()), need, _stream_handle(noisy.device))
     if st != 0:
         raise GBM3DError(st, "wiener_stage2")
     return out
@@ -339,20 +399,74 @@ def stage1_denoise(noisy, idx, n_valid, patch: int, sigma, levels: int = 3, out=
     B = noisy.shape[0] if batched else 1
     H, W = noisy.shape[-2], noisy.shape[-1]
     K = idx.shape[-1]
-    sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
-    if sig.numel() == 1:
-        sig = sig.expand(B)
-    sig = sig.contiguous().to(noisy.device)
-    if out is None:
-        out = torch.empty(noisy.shape, dtype=torch.float32, device=noisy.device)
+    tiles = ((B,) if batched else ()) + (H // patch, W // patch)
+    if patch < 1 or H % patch or W % patch or tuple(idx.shape[:-1]) != tiles:
+        raise ValueError(f"idx must be the tiling grid's table {tiles + (K,)} (stride = patch)")
+    if tuple(n_valid.shape) != tiles:
+        raise ValueError(f"n_valid must be {tiles}")
+    sig = _sigmas(sigma, B, noisy.device)
+    out = _float_out(out, noisy)
     need = int(load_library().gbm3d_stage1_workspace_bytes(B, H, W, patch, K))
-    if workspace is None:
-        workspace = torch.empty(need, dtype=torch.uint8, device=noisy.device)
-    st = load_library().gbm3d_stage1_denoise(
-        ctypes.c_void_p(noisy.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()),
-        ctypes.c_void_p(n_valid.data_ptr()), K, ctypes.c_void_p(sig.data_ptr()), levels,
-        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
-        _stream_handle(noisy.device))
+    workspace = _workspace(workspace, need, noisy.device)
+    with _on(noisy.device):
+        st = load_library().gbm3d_stage1_denoise(
+            ctypes.c_void_p(noisy.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(n_valid.data_ptr()), K, ctypes.c_void_p(sig.data_ptr()), levels,
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), need,
+            _stream_handle(noisy.device))
     if st != 0:
         raise GBM3DError(st, "stage1_denoise")
+    return out
+
+
+def _shift_array(shifts):
+    arr = (ctypes.c_int * len(shifts))(*[int(h) for h in shifts])
+    return arr, len(shifts)
+
+
+def shift_trials(img, shifts, out=None):
+    """S_h Z for every translation trial h: img int16 CUDA [(B,) H, W] ->
+    int16 [T * B, H, W] (trial-major), image t*B + b = img[b] circularly shifted by (h_t, h_t)."""
+    import torch
+    _check_cuda_int16(img, "img")
+    x = img if img.dim() == 3 else img.unsqueeze(0)
+    B, H, W = x.shape
+    arr, T = _shift_array(shifts)
+    shape = (T * B, H, W)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int16, device=img.device)
+    elif out.dtype != torch.int16 or tuple(out.shape) != shape or not out.is_contiguous() \
+            or out.device != img.device:
+        raise ValueError(f"out must be contiguous int16 {shape} on {img.device}")
+    with torch.cuda.device(img.device):
+        st = load_library().gbm3d_shift_trials(ctypes.c_void_p(x.data_ptr()), B, H, W, arr, T,
+                                               ctypes.c_void_p(out.data_ptr()),
+                                               _stream_handle(img.device))
+    if st != 0:
+        raise GBM3DError(st, "shift_trials")
+    return out
+
+
+def unshift_mean(ys, shifts, out=None):
+    """(1/T) sum_t S_-h_t(ys[t]) for trial-major float32 CUDA estimates ys [T * B, H, W]:
+    returns float32 [B, H, W]."""
+    import torch
+    if not isinstance(ys, torch.Tensor) or not ys.is_cuda or ys.dtype != torch.float32 \
+            or ys.dim() != 3 or not ys.is_contiguous():
+        raise TypeError("ys must be a contiguous CUDA float32 tensor [T*B, H, W]")
+    arr, T = _shift_array(shifts)
+    if ys.shape[0] % T:
+        raise ValueError("ys.shape[0] must be a multiple of the number of trials")
+    B, H, W = ys.shape[0] // T, ys.shape[1], ys.shape[2]
+    if out is None:
+        out = torch.empty((B, H, W), dtype=torch.float32, device=ys.device)
+    elif out.dtype != torch.float32 or tuple(out.shape) != (B, H, W) or not out.is_contiguous() \
+            or out.device != ys.device:
+        raise ValueError(f"out must be contiguous float32 {(B, H, W)} on {ys.device}")
+    with torch.cuda.device(ys.device):
+        st = load_library().gbm3d_unshift_mean(ctypes.c_void_p(ys.data_ptr()), T, B, H, W, arr,
+                                               ctypes.c_void_p(out.data_ptr()),
+                                               _stream_handle(ys.device))
+    if st != 0:
+        raise GBM3DError(st, "unshift_mean")
     return out

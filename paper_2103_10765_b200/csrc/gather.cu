@@ -257,7 +257,7 @@ extern "C" int gbm3d_gather_groups(const int16_t* imgs, int B, int H, int W, int
     if (patch > 16) return GBM3D_ERR_UNSUPPORTED;
     if (Ry == 0 || Rx == 0) return GBM3D_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (patch == 8 && K <= SLOTS && W < 65536) {
+    if (patch == 8 && K <= SLOTS && W < 65536 && H < 65536) {  // (cy << 16 | cx) slot packing
         // references per CTA: at most SLOTS / K (and 128), balanced over the row's chunks
         const int chmax = SLOTS / K < 128 ? SLOTS / K : 128;
         const int nchunk = (Rx + chmax - 1) / chmax;

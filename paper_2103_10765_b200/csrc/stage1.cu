@@ -685,7 +685,8 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
         }
     }
     {
-        const int nt = K * patch;
+        // whole warps: the TV reduction shuffles over full warps (extra threads idle)
+        const int nt = (K * patch + 31) & ~31;
         const size_t smem = ((size_t)K * patch * patch + 32 + K) * sizeof(float);
         const dim3 grid((unsigned)((H / patch) * (W / patch)), B);
         if (patch == 8 && K == 16)

@@ -1,9 +1,10 @@
 """The whole G-BM3D denoiser composed from the library's kernels (section IV-V).
 
-Every arithmetic step runs in libgbm3d.so: block matching (``block_match``), stage-1 global
-volume hard thresholding (``stage1_denoise``), stage-2 collaborative Wiener filtering
-(``wiener_stage2``).  What this module adds is the paper's schedule around them, with torch used
-only for circular shifts, rounding and averaging of whole images (plumbing):
+Every arithmetic step runs in libgbm3d.so: block matching (``block_match``), the translation
+trials' shifts and averaging (``shift_trials``, ``unshift_mean``), stage-1 global volume hard
+thresholding (``stage1_denoise``), stage-2 collaborative Wiener filtering (``wiener_stage2``).
+What this module adds is the paper's schedule around them (torch only rounds the basic estimate
+to int16 for the second matching):
 
 * stage 1: Y_f = (1/H) sum_h S_-h phi(S_h Z) over the translation trials
   h = 0, N/4, N/2 of the tiling reference grid (each trial matches its shifted image; the
@@ -19,30 +20,25 @@ from __future__ import annotations
 
 from typing import Optional, Sequence
 
-from . import block_match, stage1_denoise, wiener_stage2
+from . import block_match, shift_trials, stage1_denoise, unshift_mean, wiener_stage2
 
 
 def stage1(noisy, sigma, patch: int = 8, K: int = 16, radius: int = 16,
            trials: Optional[Sequence[int]] = None, levels: int = 3):
-    """Basic estimate (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA).  The
-    translation trials are stacked into one batch, so the matching and the global thresholding
-    each run as a single batched call over trials x images."""
+    """Basic estimate Y_f (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA).  The
+    translation trials are stacked into one batch (``shift_trials``), so the matching and the
+    global thresholding each run as a single batched call over trials x images, and
+    ``unshift_mean`` shifts the estimates back and averages them."""
     import torch
     trials = (0, patch // 4, patch // 2) if trials is None else tuple(trials)
-    dims = (-2, -1)
     x = noisy if noisy.dim() == 3 else noisy.unsqueeze(0)
     B = x.shape[0]
-    z = torch.cat([torch.roll(x, shifts=(h, h), dims=dims) if h else x for h in trials]).contiguous()
+    z = shift_trials(x, trials)
     sig = torch.as_tensor(sigma, dtype=torch.float32).reshape(-1)
     sig = (sig.expand(B) if sig.numel() == 1 else sig).repeat(len(trials))
     idx, dist, nv = block_match(z, patch, patch, radius, K, None, check=False)
     y = stage1_denoise(z, idx, nv, patch, sig, levels)
-    acc = None
-    for t, h in enumerate(trials):
-        yt = y[t * B:(t + 1) * B]
-        yt = torch.roll(yt, shifts=(-h, -h), dims=dims) if h else yt
-        acc = yt if acc is None else acc + yt
-    out = acc / len(trials)
+    out = unshift_mean(y, trials)
     return out if noisy.dim() == 3 else out[0]
 
 

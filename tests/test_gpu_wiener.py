@@ -83,9 +83,10 @@ def test_wiener_errors():
 
 def test_wiener_full_size_c3_sampled():
     """BASELINE c3's full size (2048^2, P8 s3 r19 K32, groups matched on the clean stand-in of
-    the basic estimate by the oracle): the GPU call on the whole image, checked on sampled
-    pixels whose value the oracle rebuilds from every group covering them (wiener_group of
-    each, the aggregation of PAPER.md:190 restricted to the pixel)."""
+    the basic estimate by the oracle): the GPU call on the whole image, checked on 16 windows
+    of 16 x 16 pixels (4,096 pixels: the four corners, windows across the reference-tile seams,
+    random ones) whose values the oracle rebuilds from every group with a block on the window
+    (wiener_group of each, the aggregation of PAPER.md:190 restricted to the window)."""
     cfg = CONFIGS["c3"]
     c = cfg.calls[0]
     noisy, clean, sig = make_image(cfg.H, cfg.W, cfg.n_rect, cfg.n_tex, cfg.sigma, cfg.seeds[0],
@@ -93,28 +94,30 @@ def test_wiener_full_size_c3_sampled():
     idx, dist, nv = oracle.block_match(clean, c.patch, c.stride, c.radius, c.K, c.tau)
     got = _gpu(noisy, clean.astype(np.float32), idx, nv, sig)
     H, W = noisy.shape
-    N, S, r = c.patch, c.stride, c.radius
-    gy = oracle.grid(H, N, S)
-    gx = oracle.grid(W, N, S)
+    N, WS = c.patch, 16
     rng = np.random.default_rng(7)
-    pix = [(0, 0), (H - 1, W - 1), (1000, 3)] + [tuple(int(v) for v in rng.integers(0, H, 2)) for _ in range(3)]
+    wins = [(0, 0), (0, W - WS), (H - WS, 0), (H - WS, W - WS), (40, 16), (88, 1000),
+            (1000, 2008), (2040 - WS, 500)]
+    wins += [tuple(int(v) for v in rng.integers(0, H - WS, 2)) for _ in range(16 - len(wins))]
     basic = clean.astype(np.float64)
-    for (y, x) in pix:
-        num = den = 0.0
-        ys = [i for i, v in enumerate(gy) if abs(v - y) <= r + N]
-        xs = [j for j, v in enumerate(gx) if abs(v - x) <= r + N]
-        for i in ys:
-            for j in xs:
-                cy, cx = idx[i, j] // W, idx[i, j] % W
-                ks = [k for k in range(int(nv[i, j]))
-                      if cy[k] <= y < cy[k] + N and cx[k] <= x < cx[k] + N]
-                if not ks:
-                    continue
-                Gz = np.stack([noisy[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
-                Gb = np.stack([basic[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
-                U, w = wiener.wiener_group(Gz, Gb, sig)
-                for k in ks:
-                    num += w * U[k, y - cy[k], x - cx[k]]
-                    den += w
-        assert den > 0
-        assert abs(got[y, x] - num / den) < ATOL, (y, x, got[y, x], num / den)
+    cy_all, cx_all = idx // W, idx % W
+    k_ok = np.arange(c.K)[None, None, :] < nv[..., None]
+    for (y0, x0) in wins:
+        # groups with a valid block overlapping the window
+        hit = k_ok & (cy_all <= y0 + WS - 1) & (cy_all + N > y0) & (cx_all <= x0 + WS - 1) & \
+            (cx_all + N > x0)
+        num = np.zeros((WS, WS))
+        den = np.zeros((WS, WS))
+        for i, j in zip(*np.nonzero(hit.any(axis=-1))):
+            cy, cx = cy_all[i, j], cx_all[i, j]
+            Gz = np.stack([noisy[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
+            Gb = np.stack([basic[cy[k]:cy[k] + N, cx[k]:cx[k] + N] for k in range(c.K)])
+            U, w = wiener.wiener_group(Gz, Gb, sig)
+            for k in np.nonzero(hit[i, j])[0]:
+                ya, yb = max(cy[k], y0), min(cy[k] + N, y0 + WS)
+                xa, xb = max(cx[k], x0), min(cx[k] + N, x0 + WS)
+                num[ya - y0:yb - y0, xa - x0:xb - x0] += w * U[k, ya - cy[k]:yb - cy[k], xa - cx[k]:xb - cx[k]]
+                den[ya - y0:yb - y0, xa - x0:xb - x0] += w
+        assert (den > 0).all()
+        np.testing.assert_allclose(got[y0:y0 + WS, x0:x0 + WS], num / den, atol=ATOL, rtol=0,
+                                   err_msg=f"window {(y0, x0)}")
