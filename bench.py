@@ -28,7 +28,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
-INT_LANES_PER_SM = 128      # 4 SMSP x 32 lanes issue; IADD3 (alu) + IMAD (fma) pipes, 64 each
 N_SMS = 148
 
 
@@ -220,13 +219,50 @@ def measured_peak(key, default):
         return default, "B200_PROFILING.md"
 
 
-def load_traffic(name):
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def build_id(g):
+    """Source hash the loaded libgbm3d.so was built from (gbm3d_version: "... src <id>")."""
+    v = g.version()
+    return v.split("src ")[-1].strip() if "src " in v else None
+
+
+def load_ncu(name, bid):
+    """ncu counters of the step's dominant kernel for workload `name` from the committed capture
+    profiles/ncu_counters.json, only if that capture was taken of this very build (same source
+    id); the DRAM read + write bytes of that capture are the roofline's `traffic`."""
+    path = os.path.join(ROOT, "profiles", "ncu_counters.json")
     try:
         with open(path) as f:
-            return json.load(f).get(name)
+            d = json.load(f)
     except (OSError, ValueError):
-        return None
+        return None, {"note": "no profiles/ncu_counters.json"}
+    c = d.get(name)
+    if c is None:
+        return None, {"note": f"no capture for {name}"}
+    if d.get("build") != bid:
+        return None, {"note": f"capture of build {d.get('build')}, not of this build {bid}",
+                      "stale": c}
+    out = dict(c)
+    out["build"] = bid
+    out["source"] = d.get("source", "")
+    return c.get("dram_bytes"), out
+
+
+def measure_int_peaks(g):
+    """integer instruction throughput measured in this run (the library's
+    microkernels on every SM): lane-instructions per second for the ALU pipe alone, the FMA
+    pipe alone, IMNMX, and IMAD + IADD3 mixed (the issue bound)."""
+    return {k: g.int_peak(k) / 1e12 for k in ("alu", "fma", "minmax", "mixed")}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def tensor_roofline(evals, patch, ms):
@@ -259,6 +295,9 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
 
     step()
     launches_per_step = g.last_launch_count()
+    # profiling runs (--step-only) list the step's kernels alone: no microkernels there
+    peaks = measure_int_peaks(g) if not args.step_only else {k: float("nan") for k in
+                                                             ("alu", "fma", "minmax", "mixed")}
     sampler = ClockSampler(0).start()
     times = measure_device(step, args.steps, args.warmup, flush_buf.zero_, torch)
     sampler.stop()
@@ -269,8 +308,9 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
     value = refs / (ms * 1e-3)
     A = a_eval(call.stride)
     achieved = evals * A / (ms * 1e-3) / 1e12
-    sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak = INT_LANES_PER_SM * N_SMS * sm_max * 1e6 / 1e12
+    peak = peaks["mixed"]
+    bid = build_id(g)
+    traffic, ncu = load_ncu(cfg.name, bid)
     line = {
         "metric": "ref patches matched/sec", "value": value, "unit": "refs/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -278,15 +318,19 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
         "config": workload_config(cfg, call, args),
         "gevals_per_s": evals / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TOP/s",
-                     "frac": achieved / peak, "traffic": load_traffic(cfg.name),
+                     "frac": achieved / peak, "traffic": traffic,
                      "ops_per_eval": A, "evals_per_launch": evals,
-                     "peak_basis": f"{INT_LANES_PER_SM} int32 lanes/clk/SM x {N_SMS} SMs x "
-                                   f"{sm_max:.0f} MHz (B300_MICROARCH pipe rates; DESIGN.md)",
+                     "peak_basis": "measured in this run: IMAD + IADD3 microkernel on all SMs "
+                                   "(integer issue bound, SURVEY 8(d) P_int = best measured)",
+                     "alu_pipe_peak": peaks["alu"], "frac_of_alu_pipe": achieved / peaks["alu"],
                      "model": "SURVEY 8(d) SSD-form work A_eval = 3s^2+s+1 int32 ops per "
                               "candidate evaluation (closed-form count, self excluded); the "
                               "product-form kernel moves the inner products to tcgen05, so this "
                               "is the method's ALU-roofline time bound, not an issue count",
-                     "timed": "whole step (tc16 kernel + marked-tile scan, ~3 us)"},
+                     "timed": "whole step (persistent tc16 kernel + marked-tile scan)"},
+        "int_peaks_tops": peaks,
+        "ncu": ncu,
+        "build": bid,
         "roofline_tensor": tensor_roofline(evals, call.patch, ms),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
@@ -304,10 +348,16 @@ def run_ours_single(args, cfg, call, torch, g, want_e2e=True, want_cpu=True):
         line["e2e"] = run_e2e(args, cfg, call, torch, g)
     if want_cpu:
         rate, evr, n, t, thr = oracle_sample_rate(cfg, call, args.cpu_seconds)
+        rate1, evr1, n1, t1, _ = oracle_sample_rate(cfg, call, args.cpu_seconds / 2, seed=1,
+                                                    threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": "refs/s", "cores": thr, "kind": "oracle",
                                 "sample": f"{n} random references of {cfg.name} "
                                           f"({n * evals1 / refs1:.3g} evals) in {t:.1f} s",
-                                "gevals_per_s": evr / 1e9}
+                                "gevals_per_s": evr / 1e9, "cpu_model": cpu_model(),
+                                "single_thread": {"value": rate1, "unit": "refs/s",
+                                                  "gevals_per_s": evr1 / 1e9,
+                                                  "sample": f"{n1} random references in "
+                                                            f"{t1:.1f} s, 1 thread"}}
     del imgs, outs, flush_buf
     return line
 
@@ -393,8 +443,10 @@ def run_wiener(args, cfg, call, torch, g, img, outs, flush_buf):
 def run_stage1(args, cfg, call, torch, g, img, flush_buf):
     """stage-1 global volume hard thresholding of the workload's image(s) with
     tiling references (stride = patch = 8, K = 16, the paper's K), matching included in the
-    tables but not in the timing.  HBM roofline: the fp32 volume traffic of the fused schedule
-    (DESIGN.md 7.7), about 14.5 reads/writes of the K x H x W fp32 volume per call."""
+    tables but not in the timing.  HBM roofline on ALGORITHMIC bytes: the call's inputs (image,
+    tables) and output (fp32 image), read / written once.  The method's volume of matched blocks
+    (K x H x W) does not fit on chip, so the implementation's own traffic is far larger
+    (`impl_traffic_model`: ~14.5 fp32 volume passes); both are reported."""
     N, K, levels = 8, 16, 3
     if cfg.H % 16 or cfg.W % 16:
         return None
@@ -417,7 +469,8 @@ def run_stage1(args, cfg, call, torch, g, img, flush_buf):
     # aggregation read U once (1)
     band = sum(2 / 4 ** (l - 1) for l in range(2, levels + 1))
     passes = (1 + band + 2 + band + 2) + (1 + band + 2 + band + 3) + 1
-    nbytes = passes * vol
+    impl_bytes = passes * vol
+    nbytes = img.numel() * 2 + idx.numel() * 4 + nv.numel() * 4 + out.numel() * 4
     peak, src = measured_peak("hbm_gbs", 7672.0)
     ach = nbytes / (ms * 1e-3) / 1e9
     del out, ws
@@ -425,7 +478,13 @@ def run_stage1(args, cfg, call, torch, g, img, flush_buf):
                     "spins, 1/TV weights, aggregation (tiling refs N=8, K=16)",
             "ms": ms, "pixels_per_s": cfg.B * cfg.H * cfg.W / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "bytes_per_call": nbytes, "peak_source": src}}
+                         "frac": ach / peak, "bytes_per_call": nbytes, "peak_source": src,
+                         "basis": "algorithmic bytes: image + tables in, fp32 image out"},
+            "impl_traffic_model": {"bytes_per_call": impl_bytes,
+                                   "gbs": impl_bytes / (ms * 1e-3) / 1e9,
+                                   "frac_of_hbm": impl_bytes / (ms * 1e-3) / 1e9 / peak,
+                                   "note": "~14.5 fp32 volume passes of the fused schedule "
+                                           "(DESIGN.md 7.7)"}}
 
 
 def run_denoiser(args, cfg, torch, img, flush_buf):
@@ -552,21 +611,23 @@ def run_e2e(args, cfg, call, torch, g):
             "d2h_bytes_per_step": int(sum(o.numel() * 4 for o in out))}
 
 
-def add_multi_roofline(line, cfg, call):
+def add_multi_roofline(line, cfg, call, g):
     """The N-GPU line's ALU roofline, per GPU: the closed-form evaluations over all ranks / N
-    against one GPU's derived INT32 peak, at the max-over-ranks step time (which includes the
-    c3 gather)."""
+    against rank 0's measured integer issue peak, at the max-over-ranks step time (which
+    includes the c3 gather)."""
     n = line["n_gpus"]
     ms = line["ms_per_step"]
     evals1, _ = total_evals(cfg.H, cfg.W, call.patch, call.stride, call.radius)
     evals = evals1 * cfg.B
     A = a_eval(call.stride)
-    sm_max = (line.get("clocks") or {}).get("sm_max_mhz") or 1965.0
-    peak = INT_LANES_PER_SM * N_SMS * sm_max * 1e6 / 1e12
+    peaks = measure_int_peaks(g)
+    peak = peaks["mixed"]
     achieved = evals / n * A / (ms * 1e-3) / 1e12
     line["gevals_per_s"] = evals / (ms * 1e-3) / 1e9
+    line["int_peaks_tops"] = peaks
     line["roofline"] = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TOP/s",
                         "frac": achieved / peak, "traffic": None, "ops_per_eval": A,
+                        "peak_basis": "measured on rank 0's GPU in this run (IMAD + IADD3)",
                         "per": "GPU (evaluations / N over the max-over-ranks step time)"}
 
 
@@ -603,7 +664,7 @@ def main():
         local = int(os.environ.get("LOCAL_RANK", "0"))
         line = gdist.bench_multi(args, cfg, call, sampler=ClockSampler(local))
         if line is not None and rank == 0:
-            add_multi_roofline(line, cfg, call)
+            add_multi_roofline(line, cfg, call, g)
             # the same config object as the N = 1 line and the reference arm
             line["config"] = workload_config(cfg, call, args)
             print(json.dumps(line), flush=True)
@@ -616,7 +677,7 @@ def main():
         line["also"] = {"c4": {k: also[k] for k in ("value", "unit", "ms_per_step",
                                                     "gevals_per_s", "roofline",
                                                     "roofline_tensor", "e2e", "config",
-                                                    "clocks", "gpu_launches", "gather",
+                                                    "clocks", "gpu_launches", "ncu", "gather",
                                                     "wiener", "stage1")}}
     print(json.dumps(line), flush=True)
 

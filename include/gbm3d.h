@@ -222,6 +222,18 @@ int gbm3d_block_match_host(const int16_t* h_imgs, int B, int H, int W, int patch
  * GBM3D_ERR_ARG for null pointers or n < 1. */
 int gbm3d_check_range(const int16_t* img, int64_t n, int patch, int* ok, void* stream);
 
+/* ---- Integer instruction-throughput microkernels (the ALU roofline's peak is
+ * measured on the box in the same run).  kind 0 = SHF + LOP3 (ALU pipe only), 1 = IMAD (FMA
+ * pipe only), 2 = IMNMX min/max (ALU pipe; the selection's instruction), 3 = IMAD + IADD3 (both
+ * pipes: the issue-rate bound).  gbm3d_int_peak_launch enqueues blocks x threads threads
+ * (threads a multiple of 32, <= 256), each running 8 independent chains for `iters` x 16 steps
+ * of two instructions; sink: device uint32 [blocks] (written only to keep the chains live).
+ * gbm3d_int_peak_ops returns the lane-instructions one such launch executes (0 for a bad kind).
+ * Errors: GBM3D_ERR_ARG, GBM3D_ERR_CUDA. */
+double gbm3d_int_peak_ops(int kind, int blocks, int threads, int iters);
+int gbm3d_int_peak_launch(int kind, int blocks, int threads, int iters, uint32_t* sink,
+                          void* stream);
+
 /* Number of kernel launches the last successful call on this thread enqueued (for the
  * bench's gpu_launches claim). */
 int gbm3d_last_launch_count(void);

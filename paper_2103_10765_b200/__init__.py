@@ -15,7 +15,7 @@ __all__ = [
     "TAU_NONE", "METHODS", "GBM3DError", "lib_path", "load_library", "grid_dims", "block_match",
     "block_match_rows", "block_match_host", "host_workspace_bytes", "check_range",
     "last_launch_count", "version", "gather_groups", "gather_volume", "wiener_stage2",
-    "stage1_denoise", "shift_trials", "unshift_mean",
+    "stage1_denoise", "shift_trials", "unshift_mean", "int_peak",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -71,6 +71,8 @@ def load_library():
                                       vp, ctypes.c_size_t, vp]),
         "gbm3d_shift_trials": (i32, [vp, i32, i32, i32, vp, i32, vp, vp]),
         "gbm3d_unshift_mean": (i32, [vp, i32, i32, i32, i32, vp, vp, vp]),
+        "gbm3d_int_peak_ops": (ctypes.c_double, [i32, i32, i32, i32]),
+        "gbm3d_int_peak_launch": (i32, [i32, i32, i32, i32, vp, vp]),
         "gbm3d_last_launch_count": (i32, []),
         "gbm3d_strerror": (ctypes.c_char_p, [i32]),
         "gbm3d_version": (ctypes.c_char_p, []),
@@ -470,3 +472,34 @@ def unshift_mean(ys, shifts, out=None):
     if st != 0:
         raise GBM3DError(st, "unshift_mean")
     return out
+
+
+INT_PEAK_KINDS = {"alu": 0, "fma": 1, "minmax": 2, "mixed": 3}
+
+
+def int_peak(kind: str, device=None, iters: int = 2000, reps: int = 5) -> float:
+    """Measured integer instruction throughput (lane-instructions per second) of one of the
+    library's microkernels (``INT_PEAK_KINDS``) on every SM of ``device``: 8 CTAs of 256 threads
+    per SM, CUDA-event timed, best of ``reps`` after a warm-up launch."""
+    import torch
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    k = INT_PEAK_KINDS[kind]
+    nsm = torch.cuda.get_device_properties(device).multi_processor_count
+    blocks, threads = nsm * 8, 256
+    lib = load_library()
+    sink = torch.zeros(blocks, dtype=torch.int32, device=device)
+    best = 0.0
+    with _on(device):
+        stream = torch.cuda.current_stream(device)
+        h = ctypes.c_void_p(stream.cuda_stream)
+        for rep in range(reps + 1):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            st = lib.gbm3d_int_peak_launch(k, blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), h)
+            e.record(stream)
+            if st != 0:
+                raise GBM3DError(st, "int_peak")
+            e.synchronize()
+            if rep:
+                best = max(best, lib.gbm3d_int_peak_ops(k, blocks, threads, iters) / (s.elapsed_time(e) * 1e-3))
+    return best

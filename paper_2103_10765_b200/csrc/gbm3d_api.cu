@@ -494,6 +494,10 @@ const char* gbm3d_strerror(int status) {
     }
 }
 
-const char* gbm3d_version(void) { return "gbm3d 0.1.0 (sm_100a)"; }
+#ifndef GBM3D_SRC_ID
+#define GBM3D_SRC_ID "unknown"
+#endif
+// "src <id>": the hash of the sources this library was built from (build.py source_id)
+const char* gbm3d_version(void) { return "gbm3d 0.2.0 (sm_100a) src " GBM3D_SRC_ID; }
 
 }  // extern "C"

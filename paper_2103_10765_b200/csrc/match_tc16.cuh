@@ -88,6 +88,7 @@ constexpr int NINFO = 4;         // per-tile info ring (producer -> MMA, epilogu
 constexpr int INFO_W = 8;        // words per entry: tile (-1 = no more), image, ky0, kx0, row step, skip
 constexpr int NSCHED = 64;       // tile-counter slots (concurrent launches use different slots)
 constexpr int PRO_BAR = 2;       // named barrier of the producer warps
+constexpr int MMA_PRO_BAR = 3;   // MMA warp -> producers: the tile's MMAs completed (X, A free)
 #ifndef GBM3D_TC16_BULK_MIN
 #define GBM3D_TC16_BULK_MIN 16
 #endif
@@ -260,6 +261,14 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // Dynamic tile counters: [2 * slot] = tiles handed out beyond the first wave, [2 * slot + 1] =
 // CTAs finished; the last CTA of a launch zeroes both, so each slot starts every launch at 0.
 static __device__ unsigned int g_tc16_sched[2 * tc16::NSCHED];
+
+// MMA warp, after the tile's last commit: wait until the tile's MMAs completed, then let the
+// producers (blocked on the named barrier) overwrite X and A (the whole warp arrives).
+static __device__ __forceinline__ void tc_release_producers(uint64_t* b_mma, int it, int npro,
+                                                            int lane, unsigned wm) {
+    tc::mbar_wait(b_mma, it & 1);
+    asm volatile("bar.arrive %0, %1;" ::"r"(tc16::MMA_PRO_BAR), "r"(32 * (npro + 1)) : "memory");
+}
 
 // Tile i of a call: image, first grid row and column of its 16 x 8 references.
 struct Tc16Tile {
@@ -522,7 +531,9 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
             if (tr) TC_TRP(2000 + it * 8 + 7, clock64());
             // (5) X and A, once the previous tile's MMAs no longer read them
             if (tr) TC_TRP(2000 + it * 8 + 3, clock64());
-            if (it > 0) tc::mbar_wait_long(b_mma, (it - 1) & 1, 256);
+            // wait for the MMA warp's word that the previous tile's MMAs completed: a named
+            // barrier, so the producers sleep in hardware instead of polling for a whole tile
+            if (it > 0) tc::named_bar(MMA_PRO_BAR, 32 * (NPRO + 1));
             if (tr) TC_TRP(2000 + it * 8 + 4, clock64());
             if (!skip) {
                 uint8_t* const xop = sm + g.off_x;
@@ -563,10 +574,11 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
             tc::named_bar(PRO_BAR, 32 * NPRO);  // plane reads done before the next box lands
         }
     } else if (warp == MMA_WARP) {
-        // ---------------- MMA issuer: 4 x (M128 N64 K16) per candidate row (lane 0; the whole
-        // warp when it also copies lane quarter 0's A rows into TMEM)
-        const unsigned wm = NPRO == 3 ? 0xffffffffu : 1u;
-        if (NPRO == 3 || lane == 0) {
+        // ---------------- MMA issuer: 4 x (M128 N64 K16) per candidate row (lane 0 issues; the
+        // whole warp copies lane quarter 0's A rows into TMEM when NPRO == 3 and releases the
+        // producers after each tile)
+        const unsigned wm = 0xffffffffu;
+        {
             const uint32_t idesc = tc::idesc_f16f16_f32(128, NB);
             const uint32_t xa = tc::smem_u32(sm + g.off_x);
             int s = 0;
@@ -583,6 +595,8 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                 if (skip) {
                     __syncwarp(wm);
                     if (lane == 0) tc::mbar_arrive(b_mma);
+                    __syncwarp(wm);
+                    tc_release_producers(b_mma, it, NPRO, lane, wm);
                     continue;
                 }
                 if (NPRO == 3) {  // A rows of lane quarter 0: shared buffer -> TMEM (this warp's quarter)
@@ -596,7 +610,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                     __syncwarp(wm);
                 }
                 tc::tc_fence_after();
-                if (lane == 0) {
+                // the whole warp walks the rows (converged: the waits are warp-wide), lane 0 issues
                 const int gy0 = S * ky0 - r;
                 const int t_lo = max(0, -gy0), t_hi = min(g.NT - 1, (p.H - P) - gy0);
                 RowSeq seq;
@@ -607,17 +621,20 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                     const int t = seq.next();
                     if (s >= NTS) tc::mbar_wait(&tempty[ts], ((s / NTS) - 1) & 1);
                     tc::tc_fence_after();
-                    const uint32_t bb = xa + (uint32_t)(t * XP);
+                    if (lane == 0) {
+                        const uint32_t bb = xa + (uint32_t)(t * XP);
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_f16_ts(tmem + (uint32_t)(ts * NB), tmem + TM_A + ks * 8,
-                                       tc::smem_desc(bb + ks * 2 * XP, XP, 128), idesc, ks);
-                    tc::mma_commit(&tfull[ts]);
+                        for (int ks = 0; ks < 4; ++ks)
+                            tc::mma_f16_ts(tmem + (uint32_t)(ts * NB), tmem + TM_A + ks * 8,
+                                           tc::smem_desc(bb + ks * 2 * XP, XP, 128), idesc, ks);
+                        tc::mma_commit(&tfull[ts]);
+                    }
+                    __syncwarp(wm);
                 }
-                tc::mma_commit(b_mma);  // X and A free once these MMAs completed
-                if (it < 40) TC_TRP(3000 + it * 4 + 1, clock64());
-                }
+                if (lane == 0) tc::mma_commit(b_mma);  // X and A free once these MMAs completed
+                if (lane == 0 && it < 40) TC_TRP(3000 + it * 4 + 1, clock64());
                 __syncwarp(wm);  // the warp stays converged for the next tile's TMEM copy
+                tc_release_producers(b_mma, it, NPRO, lane, wm);
             }
         }
     } else if (warp < EPI_WARPS || (EPI_HALVES == 2 && warp >= EPI_WARP1)) {

@@ -1,7 +1,7 @@
 #!/bin/bash
 # dev: new build vs round-1 build on c3/c4 timing, then the matcher parity tests
 mkdir -p gpurun_out
-for lib in paper_2103_10765_b200/libgbm3d.so variants/libgbm3d_r1.so; do
+for lib in paper_2103_10765_b200/libgbm3d.so; do
   for c in c3 c4; do
     GBM3D_LIB=$lib timeout 120 python tools/time_config.py --config $c --reps 10 2>&1 | tail -1 | sed "s|^|$lib |"
   done

@@ -43,7 +43,8 @@ out = {
     "shared_mem_per_block_bytes": scaled("launch__shared_mem_per_block_dynamic"),
     "achieved_occupancy_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "ipc_active": num("sm__inst_executed.avg.per_cycle_active"),
-    "issue_active_pct": num("sm__issue_active.avg.pct_of_peak_sustained_active"),
+    "issue_active_pct": num("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+    "inst_issued_pct": num("sm__inst_issued.avg.pct_of_peak_sustained_active"),
     "inst_executed": num("smsp__inst_executed.sum"),
     "alu_pipe_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
     "fma_pipe_pct": num("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
@@ -51,7 +52,14 @@ out = {
     "sm_clock_hz": scaled("smsp__cycles_elapsed.avg.per_second"),
     "shared_ld_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"),
     "shared_bank_conflicts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+    "shared_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+    "shared_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
 }
+# shared-memory bandwidth: every wavefront moves up to 128 B (32 banks x 4 B)
+if out["shared_wavefronts"] is not None and out["duration_s"]:
+    out["shared_gbs_upper"] = out["shared_wavefronts"] * 128 / out["duration_s"] / 1e9
+if out["dram_read_bytes"] is not None and out["duration_s"]:
+    out["dram_gbs"] = (out["dram_read_bytes"] + (out["dram_write_bytes"] or 0)) / out["duration_s"] / 1e9
 if out["dram_read_bytes"] is not None and out["dram_write_bytes"] is not None:
     out["dram_bytes"] = out["dram_read_bytes"] + out["dram_write_bytes"]
 out["units"] = {k: u.get(k) for k in ("gpu__time_duration.sum", "dram__bytes_read.sum")}
