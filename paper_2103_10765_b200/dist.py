@@ -3,12 +3,15 @@
 One process per GPU (torchrun), torch.distributed for the plumbing:
 
 * row sharding (one large image, c3): the reference grid rows are split into contiguous blocks
-  (sizes differ by <= 1).  Rank g copies only the image rows its references read -- a slab with
-  a (radius)-row halo above and (radius + patch)-row halo below, the overlapping-support
-  decomposition the paper uses for large images -- computes its rows with
-  ``gbm3d_block_match_rows`` (global raster indices), and the tables are gathered to rank 0 with
-  point-to-point NCCL transfers straight into the final [Ry, Rx, K] buffers.  The only exchange
-  step of the path is that gather.
+  of whole 16-row tiles of the tensor-core kernel (balanced in tiles; only the last block is
+  ragged).  Rank g copies only the image rows its references read -- a slab with a (radius)-row
+  halo above and (radius + patch)-row halo below, the overlapping-support decomposition the
+  paper uses for large images -- and computes its rows with
+  ``gbm3d_block_match_rows`` (global raster indices) in chunks of whole tiles on two alternating
+  compute streams.  Each chunk's tables go to rank 0 with point-to-point NCCL transfers on a
+  communication stream as soon as the chunk is done, so the gather overlaps the matching of the
+  next chunk; rank 0 computes its own rows straight into the final [Ry, Rx, K] buffers and
+  receives the others' chunks into them.  The only exchange step of the path is that gather.
 * batch split (many images, c4): images are split across ranks; no collective.
 
 Concatenating row ranges is byte-identical to one call (reading R16), so the gathered
@@ -37,15 +40,38 @@ def ref_row_y(k: int, H: int, P: int, S: int) -> int:
     return k * S if k < reg else H - P
 
 
-def row_partition(Ry: int, world: int) -> List[Tuple[int, int]]:
-    """Contiguous reference-row blocks, sizes differing by at most one."""
-    base, extra = divmod(Ry, world)
+TILE_ROWS = 16  # reference rows of one tensor-core tile (match_tc16.cuh TY)
+
+
+def row_partition(Ry: int, world: int, align: int = 1) -> List[Tuple[int, int]]:
+    """Contiguous reference-row blocks covering [0, Ry).  ``align`` = 1: sizes differ by at most
+    one.  ``align`` > 1 (the matcher's tile height): blocks are whole multiples of ``align`` rows
+    (only the last block may be ragged) with tile counts differing by at most one, so no rank
+    pays for partial tiles in the middle of the image."""
+    if align <= 1:
+        base, extra = divmod(Ry, world)
+        sizes = [base + (1 if g < extra else 0) for g in range(world)]
+    else:
+        nt = -(-Ry // align)
+        base, extra = divmod(nt, world)
+        sizes = [(base + (1 if g < extra else 0)) * align for g in range(world)]
     out, a = [], 0
-    for g in range(world):
-        b = a + base + (1 if g < extra else 0)
+    for sz in sizes:
+        b = min(Ry, a + sz)
         out.append((a, b))
         a = b
     return out
+
+
+def chunk_rows(k0: int, k1: int, nchunk: int, align: int = TILE_ROWS) -> List[Tuple[int, int]]:
+    """Split [k0, k1) into at most ``nchunk`` pieces of whole ``align``-row tiles (the last one
+    may be ragged): the granules of the overlapped gather."""
+    n = k1 - k0
+    if n <= 0:
+        return []
+    per = -(-n // max(1, nchunk))             # ceil(n / nchunk) rows per chunk
+    step = -(-per // align) * align           # rounded up to whole tiles
+    return [(a, min(k1, a + step)) for a in range(k0, k1, step)]
 
 
 def slab_bounds(H: int, P: int, S: int, r: int, k0: int, k1: int) -> Tuple[int, int]:
@@ -89,6 +115,92 @@ def gather_rows(parts: Sequence[torch.Tensor], full: torch.Tensor | None, ranges
             req.wait()
 
 
+def gather_rows_chunked(compute, parts, full, ranges, rank: int, world: int, nchunk: int,
+                        dst: int = 0, streams=None, host=None):
+    """Compute this rank's reference rows chunk by chunk and gather them to ``dst`` while the
+    next chunk is being computed.
+
+    ``compute(a, b, outs)`` fills global rows [a, b) of every table into the views ``outs``.
+    On ``dst`` the views are slices of the full tables ``full`` (its own rows land in place);
+    elsewhere they are slices of the local tables ``parts`` (first dim = the rank's rows), and
+    each finished chunk is sent to ``dst``, which receives every other rank's chunks straight
+    into ``full``.  Chunks are whole tiles (``chunk_rows``) and deterministic on every rank, so
+    the point-to-point ops pair up in order.  With CUDA ``streams`` = (compute0, compute1, comm)
+    chunks alternate between the two compute streams (consecutive chunk kernels overlap on the
+    SMs) and the transfers run on the comm stream after an event per chunk: the gather overlaps
+    the matching (NCCL over NVLink).  Without streams (gloo / CPU) every step is synchronous.
+    ``host`` (dst only, with streams): pinned host tables shaped like ``full``; every chunk is
+    copied out as soon as it is complete there (own chunks after their kernel, received chunks
+    after their transfer), so the copy to the host overlaps the rest of the step."""
+    my = ranges[rank]
+    mine = chunk_rows(my[0], my[1], nchunk)
+    reqs = []
+
+    def views(a, b):
+        if rank == dst:
+            return tuple(f[a:b] for f in full)
+        return tuple(t[a - my[0]:b - my[0]] for t in parts)
+
+    if rank == dst:
+        recv_plan = {g: chunk_rows(ranges[g][0], ranges[g][1], nchunk) for g in range(world)
+                     if g != dst}
+        nmax = max([len(mine)] + [len(v) for v in recv_plan.values()])
+    else:
+        nmax = len(mine)
+    cur = torch.cuda.current_stream() if streams else None
+    if streams:
+        for st in streams[:2]:
+            st.wait_stream(cur)  # the inputs are ready on the caller's stream
+    for c in range(nmax):
+        ev = None
+        if c < len(mine):
+            a, b = mine[c]
+            outs = views(a, b)
+            if streams:
+                with torch.cuda.stream(streams[c & 1]):
+                    compute(a, b, outs)
+                    if host is not None and rank == dst:
+                        for h, o in zip(host, outs):
+                            h[a:b].copy_(o, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(streams[c & 1])
+            else:
+                compute(a, b, outs)
+        ops = []
+        if rank == dst:
+            for g, plan in recv_plan.items():
+                if c < len(plan):
+                    a, b = plan[c]
+                    ops += [dist.P2POp(dist.irecv, f[a:b], g) for f in full]
+        elif ev is not None or (not streams and c < len(mine)):
+            a, b = mine[c]
+            ops += [dist.P2POp(dist.isend, v, dst) for v in views(a, b)]
+        if ops:
+            if streams:
+                if ev is not None:
+                    streams[2].wait_event(ev)
+                with torch.cuda.stream(streams[2]):
+                    got = dist.batch_isend_irecv(ops)
+                    reqs += got
+                    if host is not None and rank == dst:
+                        for r in got:
+                            r.wait()  # the comm stream now follows the received chunk
+                        for g, plan in recv_plan.items():
+                            if c < len(plan):
+                                a, b = plan[c]
+                                for h, f in zip(host, full):
+                                    h[a:b].copy_(f[a:b], non_blocking=True)
+            else:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+    if streams:
+        with torch.cuda.stream(streams[2]):
+            for r in reqs:
+                r.wait()
+        for st in streams:
+            cur.wait_stream(st)
+
+
 def block_match_rowsharded(img_rows: torch.Tensor, slab_y0: int, H: int, W: int, patch: int,
                            stride: int, radius: int, K: int, tau, rank: int, world: int,
                            gather: bool = True):
@@ -97,7 +209,7 @@ def block_match_rowsharded(img_rows: torch.Tensor, slab_y0: int, H: int, W: int,
     rank 0 (None elsewhere) when ``gather``, else this rank's block and its row range."""
     import paper_2103_10765_b200 as g
     Ry, Rx = g.grid_dims(H, W, patch, stride)
-    ranges = row_partition(Ry, world)
+    ranges = row_partition(Ry, world, TILE_ROWS)
     k0, k1 = ranges[rank]
     y0, y1 = slab_bounds(H, patch, stride, radius, k0, k1)
     slab = img_rows[y0 - slab_y0:y1 - slab_y0].contiguous()
@@ -127,11 +239,10 @@ def _init():
 
 def _e2e_bytes(cfg, call, Ry, Rx, world):
     """Bytes per step over all ranks: the slabs (with their halo rows) or images in, the tables
-    out (idx, dist int32 [.., K] and n_valid int32)."""
+    out (idx, dist int32 [.., K] and n_valid int32; for c3 the full table, on rank 0)."""
     if cfg.B == 1:
-        ranges = row_partition(Ry, world)
         rows_in = 0
-        for k0, k1 in ranges:
+        for k0, k1 in row_partition(Ry, world, TILE_ROWS):
             y0, y1 = slab_bounds(cfg.H, call.patch, call.stride, call.radius, k0, k1)
             rows_in += y1 - y0
         h2d = rows_in * cfg.W * 2
@@ -141,57 +252,63 @@ def _e2e_bytes(cfg, call, Ry, Rx, world):
     return {"h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
+def _sharded_step(g, cfg, call, slab, y0, ranges, rank, world, local_out, full, streams,
+                  nchunk=3, host=None):
+    """One row-sharded matching step: this rank's rows in tile chunks, each gathered to rank 0
+    while the next is matched (gather_rows_chunked); with ``host``, rank 0 also copies every
+    completed chunk to those pinned host tables."""
+    def compute(a, b, outs):
+        g.block_match_rows(slab, y0, cfg.H, cfg.W, call.patch, call.stride, call.radius, call.K,
+                           call.tau, a, b, out=outs)
+    gather_rows_chunked(compute, local_out, full, ranges, rank, world, nchunk, streams=streams,
+                        host=host)
+
+
 def _e2e_multi(args, cfg, call, g, dev, rank, world, sharded):
-    """Per-step wall time (ms, max over ranks) of host input -> match -> host tables."""
+    """Per-step wall time (ms, max over ranks) of host input -> match -> host tables.  c3: every
+    rank copies its pinned slab in, matches its rows with the chunked gather, and rank 0 copies
+    the FULL table back to pinned host memory; c4: every rank runs the pipelined host entry on
+    its images (its tables come back to its host)."""
     from synth import config_images
     Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
     if sharded:
         img = torch.from_numpy(config_images(cfg)[0])
-        k0, k1 = row_partition(Ry, world)[rank]
+        ranges = row_partition(Ry, world, TILE_ROWS)
+        k0, k1 = ranges[rank]
         y0, y1 = slab_bounds(cfg.H, call.patch, call.stride, call.radius, k0, k1)
         h_in = img[y0:y1].contiguous().pin_memory()
-        n_img, rows = 1, k1 - k0
+        d_in = torch.empty(h_in.shape, dtype=h_in.dtype, device=dev)
+        local_out = (torch.empty((k1 - k0, Rx, call.K), dtype=torch.int32, device=dev),
+                     torch.empty((k1 - k0, Rx, call.K), dtype=torch.int32, device=dev),
+                     torch.empty((k1 - k0, Rx), dtype=torch.int32, device=dev))
+        full = h_out = None
+        if rank == 0:
+            full = (torch.empty((Ry, Rx, call.K), dtype=torch.int32, device=dev),
+                    torch.empty((Ry, Rx, call.K), dtype=torch.int32, device=dev),
+                    torch.empty((Ry, Rx), dtype=torch.int32, device=dev))
+            h_out = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in full)
+        streams = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
     else:
         b0, b1 = batch_partition(cfg.B, world)[rank]
         h_in = torch.from_numpy(config_images(cfg)[b0:b1]).pin_memory()
-        n_img, rows = b1 - b0, Ry
-    shape = (n_img, rows, Rx) if not sharded else (rows, Rx)
-    h_out = (torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
-             torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
-             torch.empty(shape, dtype=torch.int32, pin_memory=True))
-    d_out = tuple(torch.empty_like(t, device=dev) for t in h_out)
-    ws = None
-    if not sharded:
+        n_img = b1 - b0
+        shape = (n_img, Ry, Rx)
+        h_out = (torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
+                 torch.empty(shape + (call.K,), dtype=torch.int32, pin_memory=True),
+                 torch.empty(shape, dtype=torch.int32, pin_memory=True))
         ws = torch.empty(g.host_workspace_bytes(n_img, cfg.H, cfg.W, call.patch, call.stride,
                                                 call.K), dtype=torch.uint8, device=dev)
 
-    d_in = torch.empty(h_in.shape, dtype=h_in.dtype, device=dev)
-    copy_stream = torch.cuda.Stream(device=dev)
-    # row chunks of the rank's range (multiples of 16 rows): the copy of chunk c's tables
-    # overlaps the matching of chunk c + 1
-    nck = max(1, min(6, rows // 32))
-    stepr = ((rows + nck - 1) // nck + 15) // 16 * 16
-    chunks = [(a, min(rows, a + stepr)) for a in range(0, rows, stepr)]
-
     def step():
         if sharded:
-            comp = torch.cuda.current_stream(dev)
-            with torch.cuda.stream(copy_stream):
-                d_in.copy_(h_in, non_blocking=True)
-            comp.wait_stream(copy_stream)
-            for a, b in chunks:
-                dv = tuple(t[a:b] for t in d_out)
-                g.block_match_rows(d_in, y0, cfg.H, cfg.W, call.patch, call.stride, call.radius,
-                                   call.K, call.tau, k0 + a, k0 + b, out=dv)
-                copy_stream.wait_stream(comp)
-                with torch.cuda.stream(copy_stream):
-                    for h, d in zip(h_out, dv):
-                        h[a:b].copy_(d, non_blocking=True)
-            copy_stream.synchronize()
+            d_in.copy_(h_in, non_blocking=True)
+            _sharded_step(g, cfg, call, d_in, y0, ranges, rank, world, local_out, full, streams,
+                          nchunk=6, host=h_out)
+            torch.cuda.current_stream(dev).synchronize()
         else:
             # the pipelined host-buffer entry (copies overlapped with the matching)
             g.block_match_host(h_in, call.patch, call.stride, call.radius, call.K, call.tau,
-                               workspace=ws, out=h_out)
+                               workspace=ws, out=h_out, device=dev)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -224,7 +341,7 @@ def bench_multi(args, cfg, call, sampler=None):
     Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
     if sharded:
         img = torch.from_numpy(config_images(cfg)[0])
-        ranges = row_partition(Ry, world)
+        ranges = row_partition(Ry, world, TILE_ROWS)
         k0, k1 = ranges[rank]
         y0, y1 = slab_bounds(cfg.H, call.patch, call.stride, call.radius, k0, k1)
         slab = img[y0:y1].contiguous().to(dev)
@@ -236,11 +353,10 @@ def bench_multi(args, cfg, call, sampler=None):
             full = (torch.empty((Ry, Rx, call.K), dtype=torch.int32, device=dev),
                     torch.empty((Ry, Rx, call.K), dtype=torch.int32, device=dev),
                     torch.empty((Ry, Rx), dtype=torch.int32, device=dev))
+        streams = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
 
         def step():
-            g.block_match_rows(slab, y0, cfg.H, cfg.W, call.patch, call.stride, call.radius,
-                               call.K, call.tau, k0, k1, out=local_out)
-            gather_rows(local_out, full, ranges, rank, world)
+            _sharded_step(g, cfg, call, slab, y0, ranges, rank, world, local_out, full, streams)
         my_refs = (k1 - k0) * Rx
     else:
         ranges = batch_partition(cfg.B, world)
@@ -307,8 +423,10 @@ def bench_multi(args, cfg, call, sampler=None):
         if e2e_ms is not None:
             line["e2e"] = {"value": total_refs / (e2e_ms * 1e-3), "unit": "refs/s",
                            "ms_per_step": e2e_ms, **_e2e_bytes(cfg, call, Ry, Rx, world),
-                           "note": "per rank: pinned H2D of its input, match, D2H of its "
-                                   "tables; wall clock, max over ranks"}
+                           "note": ("c3: pinned H2D of every rank's slab, chunked match + "
+                                    "gather, D2H of the full table on rank 0" if sharded else
+                                    "per rank: the pipelined host entry on its images") +
+                                   "; wall clock, max over ranks"}
         cl = [c for c in all_clocks if c]
         if cl:
             mhz = [c["sm_mhz"] for c in cl if c.get("sm_mhz")]
