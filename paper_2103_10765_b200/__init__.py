@@ -78,7 +78,12 @@ def load_library():
         "gbm3d_version": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if os.environ.get("GBM3D_LIB"):  # dev builds of older sources: call-time error
+                continue
+            raise
         fn.restype = res
         fn.argtypes = args
     _lib = lib

@@ -109,17 +109,12 @@ static int make_params(MatchParams& p, int B, int H, int W, int patch, int strid
 static cudaError_t launch_direct(const MatchParams& p, cudaStream_t st, int k_begin, int k_end,
                                  int m_begin, int m_end, int* launches) {
     if (k_end <= k_begin || m_end <= m_begin) return cudaSuccess;
-    const long long wy = std::min(p.side, p.H - p.P + 1), wx = std::min(p.side, p.W - p.P + 1);
-    int npow2 = 1;
-    while (npow2 < wy * wx) npow2 <<= 1;
-    if (npow2 < 2) npow2 = 2;
-    const int smem = npow2 * 8;
-    cudaError_t e = cudaFuncSetAttribute(match_direct_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    // compile-time patch for the common shapes (unrolled rows), any P <= 16 otherwise
+    auto kern = p.P == 8 ? match_direct_kernel<8> : p.P == 12 ? match_direct_kernel<12>
+              : p.P == 16 ? match_direct_kernel<16> : match_direct_kernel<0>;
     const long long nref = (long long)(k_end - k_begin) * (m_end - m_begin);
     dim3 grid((unsigned)nref, 1, p.B);
-    match_direct_kernel<<<grid, 256, smem, st>>>(p, k_begin, m_begin, m_end - m_begin, npow2);
+    kern<<<grid, DIRECT_THREADS, 0, st>>>(p, k_begin, m_begin, m_end - m_begin);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
