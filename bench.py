@@ -509,7 +509,7 @@ def run_denoiser(args, cfg, torch, img, flush_buf):
     y = out["y"].double().cpu().numpy()
     noisy = img.double().cpu().numpy()
     psnr = lambda a: float(10 * np.log10(255.0 ** 2 / np.mean((a - clean) ** 2)))
-    return {"what": "denoise(): G-BM3D2 = stage 1 (3 trials: P8 s8 K16 r16 matching + global "
+    return {"what": "denoise(): G-BM3D2 = stage 1 (3 trials: P16 s16 K16 r16 matching + global "
                     "volume thresholding) + stage 2 (P8 s3 K32 r16 matching on the basic "
                     "estimate + Wiener), synthetic image",
             "ms": ms, "psnr_noisy_db": psnr(noisy), "psnr_out_db": psnr(y),

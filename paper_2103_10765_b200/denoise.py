@@ -12,9 +12,10 @@ to int16 for the second matching):
 * stage 2: matching on the basic estimate (rounded to int16), Wiener
   filtering of the noisy image's groups with the basic estimate's spectra, aggregation.
 
-Parameters default to the paper's except where the library's shapes differ
-(DESIGN.md): stage 1 uses N = 8 tiles with K = 16, stage 2 N = 8 blocks on a stride-3 grid with
-K = 32, both with a search radius of 16 (the paper's window "32").
+Parameters default to the paper's: stage 1 uses N = 16 tiles with K = 16 and
+the trials h = 0, N/4, N/2, stage 2 N = 8 blocks on a stride-3 grid with K = 32 (the
+library's choice: the paper's stage-2 reference blocks tile the image), both with a search
+radius of 16 (the paper's window "32").  ``stage1(patch=8)`` gives the N = 8 variant.
 """
 from __future__ import annotations
 
@@ -23,7 +24,7 @@ from typing import Optional, Sequence
 from . import block_match, shift_trials, stage1_denoise, unshift_mean, wiener_stage2
 
 
-def stage1(noisy, sigma, patch: int = 8, K: int = 16, radius: int = 16,
+def stage1(noisy, sigma, patch: int = 16, K: int = 16, radius: int = 16,
            trials: Optional[Sequence[int]] = None, levels: int = 3):
     """Basic estimate Y_f (float32, same shape as ``noisy`` [(B,) H, W] int16 CUDA).  The
     translation trials are stacked into one batch (``shift_trials``), so the matching and the

@@ -34,9 +34,9 @@ def test_single_trial_is_one_call():
     from paper_2103_10765_b200 import denoise as dn
     noisy, clean, sig = make_image(64, 64, 6, 2, 25.0, 3, return_clean=True)
     z = torch.from_numpy(noisy).cuda()
-    a = dn.stage1(z, sig, trials=(0,))
-    idx, dist, nv = g.block_match(z, 8, 8, 16, 16, None)
-    b = g.stage1_denoise(z, idx, nv, 8, sig)
+    a = dn.stage1(z, sig, trials=(0,))           # the paper's N = 16 tiles
+    idx, dist, nv = g.block_match(z, 16, 16, 16, 16, None)
+    b = g.stage1_denoise(z, idx, nv, 16, sig)
     torch.cuda.synchronize()
     # equal up to the order of the fp32 atomic reductions in the aggregation (run to run)
     np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), atol=1e-3, rtol=0)
