@@ -27,6 +27,10 @@
 //     gates.  At the end an in-place heapsort orders each heap and the strip writes the tables
 //     with coalesced 128-byte rows.
 #pragma once
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gbm3d {
@@ -277,8 +281,11 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
     return cnt;
 }
 
+// nsplit > 1 (small images): the CTAs of a cluster of nsplit along z share one strip tile and
+// take interleaved subsets of the displacement blocks; cluster rank 0 merges the others' sorted
+// heaps through distributed shared memory and writes the tables (more CTAs fill the GPU).
 template <class Cfg>
-__global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS) {
+__global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS, int nsplit) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
     constexpr int RC = Cfg::RC, CB = Cfg::CB, WPS = Cfg::WPS, HALF = TRY / WPS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int strip = warp / WPS, half = warp % WPS;
-    const int b = blockIdx.z;
+    const int b = (int)blockIdx.z / nsplit, split = (int)blockIdx.z % nsplit;
     const int kr0 = p.row_begin, kr1 = min(p.row_end, p.Ry_reg);  // regular rows in this call
     const int k0 = kr0 + (int)blockIdx.y * TRY * NS;
     const int m0 = (int)blockIdx.x * RC;
@@ -323,7 +330,9 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     const int m = m0 + lane;
     const int nk = min(TRY, kr1 - kw);
     const int nm = min(RC, p.Rx_reg - m0);
-    if (nk <= 0 || nm <= 0) return;  // strip without references (only pair barriers follow)
+    // strip without references (only pair barriers follow); with a split it still walks the
+    // loop (no passes) so that every thread reaches the cluster barriers
+    if ((nk <= 0 || nm <= 0) && nsplit == 1) return;
     const bool lane_ok = (lane < RC) && (m < p.Rx_reg);
 
     const int arow0 = r + S * TRY * strip;  // smem row of strip row 0
@@ -352,10 +361,11 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
     const uint32_t side = (uint32_t)p.side;
     const int nDY = (p.side + D - 1) / D;
     const int NB = p.side * nDY;  // displacement blocks (dx-major)
+    const int NBs = (NB + nsplit - 1) / nsplit;  // this CTA's blocks: every nsplit-th
 
     if (L > 0) {
-        for (int it = 0; it < NB; it += WPS) {
-            const int blk = it + half;
+        for (int it = 0; it < NBs; it += WPS) {
+            const int blk = (it + half) * nsplit + split;
             if (blk < NB) {
                 // centre-out visiting order (dx: 0, +1, -1, +2, ...; dy blocks likewise): the
                 // nearest displacements usually match best, so the heap gates tighten early
@@ -503,6 +513,39 @@ __global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS)
             if (refok[k]) heap_sort(heap0 + k * LP * HEAP_STRIDE, LP);
         if (WPS == 2) pair_sync(strip); else __syncwarp();
     }
+    if (nsplit > 1) {
+        // rank 0 keeps, per reference, the L smallest of its sorted list and the other ranks'
+        // (distinct displacements: distinct keys), read through distributed shared memory; the
+        // merged list goes through this lane's queue slots (L <= TRY D, checked on the host)
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        if (split == 0 && L > 0) {
+            const int off0 = LP - L;
+#pragma unroll 1
+            for (int k = half; k < nk; k += WPS) {
+                if (!refok[k]) continue;
+                uint32_t* const mine = heap0 + (k * LP + off0) * HEAP_STRIDE;
+#pragma unroll 1
+                for (int rk = 1; rk < nsplit; ++rk) {
+                    const uint32_t* peer = cl.map_shared_rank(mine, rk);
+                    int ia = 0, ib = 0;
+#pragma unroll 1
+                    for (int o = 0; o < L; ++o) {
+                        const uint32_t va = mine[ia * HEAP_STRIDE], vb = peer[ib * HEAP_STRIDE];
+                        const bool ta = va < vb;
+                        qw[o * 32] = ta ? va : vb;
+                        ia += ta ? 1 : 0;
+                        ib += ta ? 0 : 1;
+                    }
+#pragma unroll 1
+                    for (int o = 0; o < L; ++o) mine[o * HEAP_STRIDE] = qw[o * 32];
+                }
+            }
+        }
+        cl.sync();  // the other ranks' heaps are read: they may exit
+        if (split != 0 || nk <= 0) return;
+    }
 
     // ---- epilogue: coalesced rows; slot 0 = self (d = 0), ranks 1.. sorted keys, pads (self,-1)
     const uint32_t cmask = (1u << CB) - 1u;
@@ -586,7 +629,46 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     if (e != cudaSuccess) return e;
     dim3 grid((p.Rx_reg + Cfg::RC - 1) / Cfg::RC,
               (kr1 - kr0 + Cfg::TRY * best_ns - 1) / (Cfg::TRY * best_ns), p.B);
-    kern<<<grid, 32 * Cfg::WPS * best_ns, best_smem, stream>>>(p, best_ns);
+    // a grid that fills less than half the GPU's resident warps (small images): split the
+    // displacement blocks over a cluster of CTAs per tile (the merge needs L <= TRY D and the
+    // 32-bit keys to be exact, i.e. no 64-bit fallback)
+    int n_sm = 0;
+    e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    const long long ctas = (long long)grid.x * grid.y * grid.z;
+    const long long cap = (long long)n_sm * (best_warps / (Cfg::WPS * best_ns));
+    int nsplit = 1;
+    if (!p.tau_above_dsat && p.K - 1 <= Cfg::TRY * Cfg::D && ctas < cap) {
+        // about 1.5 waves of the resident CTA slots (measured on c2: 1.5 -> 3 splits, 0.38 ->
+        // 0.31 ms; 2 / 4 / 6 / 8 splits 0.33 / 0.34 / 0.40 / 0.47 ms)
+        nsplit = (int)((3 * cap + 2 * ctas - 1) / (2 * ctas));
+        nsplit = nsplit > 4 ? 4 : nsplit;
+    }
+    static const int split_env = getenv("GBM3D_STRIP_SPLIT") ? atoi(getenv("GBM3D_STRIP_SPLIT")) : 0;
+    if (split_env > 0 && !p.tau_above_dsat && p.K - 1 <= Cfg::TRY * Cfg::D) nsplit = split_env;  // dev
+    static const bool dbg = getenv("GBM3D_DEBUG") != nullptr;
+    if (dbg)
+        fprintf(stderr, "gbm3d: strip P%d S%d grid %u x %u x %u, %d strips/CTA, %lld CTAs, cap %lld, split %d\n",
+                Cfg::P, Cfg::S, grid.x, grid.y, grid.z, best_ns, ctas, cap, nsplit);
+    if (nsplit == 1) {
+        kern<<<grid, 32 * Cfg::WPS * best_ns, best_smem, stream>>>(p, best_ns, 1);
+    } else {
+        grid.z *= nsplit;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(32 * Cfg::WPS * best_ns);
+        cfg.dynamicSmemBytes = best_smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = nsplit;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, p, best_ns, nsplit);
+        if (e != cudaSuccess) return e;
+    }
     if (launches) ++*launches;
     return cudaGetLastError();
 }
