@@ -201,6 +201,16 @@ int gbm3d_shift_trials(const int16_t* imgs, int B, int H, int W, const int* shif
 int gbm3d_unshift_mean(const float* ys, int T, int B, int H, int W, const int* shifts,
                        float* out, void* stream);
 
+/* Test hook of the same operation: additionally writes Upsilon's keep (1) / zero (0) decision for
+ * every coefficient of both cycle spins to keep: device uint8 [2][B][K][H][W] in the in-place
+ * layout of the transform (spatial Mallat layout, Haar positions along the group), so that a
+ * float64 evaluation can take the same decisions for the coefficients that lie within rounding
+ * of their threshold.  Same errors as gbm3d_stage1_denoise (GBM3D_ERR_ARG for a null keep). */
+int gbm3d_stage1_denoise_keep(const int16_t* noisy, int B, int H, int W, int patch,
+                              const int32_t* idx, const int32_t* n_valid, int K,
+                              const float* sigmas, int levels, float* out, void* workspace,
+                              size_t workspace_bytes, uint8_t* keep, void* stream);
+
 /* Host-buffer entry (end-to-end path): h_imgs is HOST int16 [B][H][W] (pinned for async
  * copies), outputs are HOST int32 arrays with the batched layouts.  d_workspace is a device
  * buffer of at least gbm3d_host_workspace_bytes(...) bytes.  Copies in, matches, copies out,

@@ -49,11 +49,12 @@ def idwt1(a: np.ndarray, d: np.ndarray, axis: int) -> np.ndarray:
     half = a.shape[0]
     M = 2 * half
     x = np.zeros((M,) + a.shape[1:])
-    for k in range(half):
-        for n, v in H_SY.items():
-            x[(2 * k + n) % M] += v * a[k]
-        for n, v in G_SY.items():
-            x[(2 * k + n) % M] += v * d[k]
+    k = np.arange(half)
+    # for a fixed tap n the targets (2k + n) mod M, k < M/2, are distinct: one vector update each
+    for n, v in H_SY.items():
+        x[(2 * k + n) % M] += v * a
+    for n, v in G_SY.items():
+        x[(2 * k + n) % M] += v * d
     return np.moveaxis(x, 0, axis)
 
 
@@ -112,11 +113,15 @@ def spatial_level_map(H: int, W: int, levels: int) -> np.ndarray:
     return lev
 
 
-def upsilon(T: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
+def upsilon(T: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0,
+            override=None) -> np.ndarray:
     """Upsilon on a coefficient volume T [K, H, W] in the in-place layout: keep |alpha| >= lambda
      with lambda_l = sigma (3.6 - 0.3 l) for the spatial level l of the
     coefficient (the final LL band counts as level L); the coefficients that are
-    approximations both in space (LL_L) and along z are always kept (reading S2)."""
+    approximations both in space (LL_L) and along z are always kept (reading S2).
+    ``override`` (tests only): (mask, keep) boolean arrays shaped like T; where mask is set the
+    decision is taken from keep -- used to follow a second implementation's decisions on the
+    coefficients that lie within rounding of their threshold (no arithmetic changes)."""
     K, H, W = T.shape
     lz = min(levels, int(math.log2(K)))
     lev = spatial_level_map(H, W, levels)
@@ -126,16 +131,25 @@ def upsilon(T: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) ->
     zapprox = np.zeros(K, dtype=bool)
     zapprox[:: 1 << lz] = True
     keep[np.ix_(zapprox, np.arange(hL), np.arange(wL))] = True
+    if override is not None:
+        keep = np.where(override[0], override[1], keep)
     return np.where(keep, T, 0.0)
 
 
-def w3d_threshold(V: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0) -> np.ndarray:
+def w3d_threshold(V: np.ndarray, sigma: float, levels: int, lam_scale: float = 1.0,
+                  override=None) -> np.ndarray:
     """T3D^-1( Upsilon( T3D(V) ) ) for one volume V [K, H, W] (readings S1, S2).  `lam_scale`
     (tests only) scales the thresholds, to find the decisions that sit within rounding of them."""
     K = V.shape[0]
     lz = min(levels, int(math.log2(K)))
     T = haar_z(dwt2(V, levels), lz)
-    return idwt2(haar_z(upsilon(T, sigma, levels, lam_scale), lz, inverse=True), levels)
+    return idwt2(haar_z(upsilon(T, sigma, levels, lam_scale, override), lz, inverse=True), levels)
+
+
+def spin_coefficients(V: np.ndarray, h: int, levels: int = 3) -> np.ndarray:
+    """Tests only: the coefficients T3D(S_h V) that Upsilon sees in cycle spin h."""
+    lz = min(levels, int(math.log2(V.shape[0])))
+    return haar_z(dwt2(np.roll(V, (h, h, h), axis=(0, 1, 2)), levels), lz)
 
 
 def threshold_margin(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)) -> float:
@@ -157,13 +171,14 @@ def threshold_margin(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1)
 
 
 def filter_volume(V: np.ndarray, sigma: float, levels: int = 3, shifts=(0, 1),
-                  lam_scale: float = 1.0) -> np.ndarray:
+                  lam_scale: float = 1.0, overrides=None) -> np.ndarray:
     """U = (1/H) sum_h S_-h( T3D^-1 Upsilon T3D (S_h V) ), S_h = circular shift by h along all
     three axes (reading S3)."""
     acc = np.zeros(V.shape)
-    for h in shifts:
+    for i, h in enumerate(shifts):
         Vh = np.roll(V, (h, h, h), axis=(0, 1, 2))
-        acc += np.roll(w3d_threshold(Vh, sigma, levels, lam_scale), (-h, -h, -h), axis=(0, 1, 2))
+        ov = overrides[i] if overrides is not None else None
+        acc += np.roll(w3d_threshold(Vh, sigma, levels, lam_scale, ov), (-h, -h, -h), axis=(0, 1, 2))
     return acc / len(shifts)
 
 
@@ -175,13 +190,13 @@ def tv3d(G: np.ndarray) -> float:
 
 
 def stage1(noisy: np.ndarray, idx: np.ndarray, n_valid: np.ndarray, patch: int, sigma: float,
-           levels: int = 3, shifts=(0, 1), lam_scale: float = 1.0) -> np.ndarray:
+           levels: int = 3, shifts=(0, 1), lam_scale: float = 1.0, overrides=None) -> np.ndarray:
     """phi(Z) for tiling references (stride = N): the filtered volume's groups are aggregated
     at their blocks' positions with weights 1 / TV, first n_valid blocks."""
     H, W = noisy.shape
     N = patch
     V = oracle.gather_volume(noisy, idx, N).astype(np.float64)   # [K, H, W]
-    U = filter_volume(V, sigma, levels, shifts, lam_scale)
+    U = filter_volume(V, sigma, levels, shifts, lam_scale, overrides)
     Ry, Rx, K = idx.shape
     num = np.zeros((H, W))
     den = np.zeros((H, W))

@@ -67,6 +67,8 @@ def load_library():
         "gbm3d_stage1_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32, i32, i32]),
         "gbm3d_stage1_denoise": (i32, [vp, i32, i32, i32, i32, vp, vp, i32, vp, i32, vp, vp,
                                        ctypes.c_size_t, vp]),
+        "gbm3d_stage1_denoise_keep": (i32, [vp, i32, i32, i32, i32, vp, vp, i32, vp, i32, vp, vp,
+                                            ctypes.c_size_t, vp, vp]),
         "gbm3d_wiener_stage2": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp,
                                       vp, ctypes.c_size_t, vp]),
         "gbm3d_shift_trials": (i32, [vp, i32, i32, i32, vp, i32, vp, vp]),
@@ -394,7 +396,7 @@ def wiener_stage2(noisy, basic, idx, n_valid, patch: int, sigma, out=None, works
 
 
 def stage1_denoise(noisy, idx, n_valid, patch: int, sigma, levels: int = 3, out=None,
-                   workspace=None):
+                   workspace=None, keep=None):
     """Stage-1 global volume hard thresholding: noisy int16
     CUDA [(B,) H, W], tables of ``block_match(noisy, patch, patch, ...)`` (tiling references).
     Returns the float32 estimate [(B,) H, W]."""
@@ -415,12 +417,19 @@ def stage1_denoise(noisy, idx, n_valid, patch: int, sigma, levels: int = 3, out=
     out = _float_out(out, noisy)
     need = int(load_library().gbm3d_stage1_workspace_bytes(B, H, W, patch, K))
     workspace = _workspace(workspace, need, noisy.device)
+    if keep is not None:  # test hook: Upsilon's decisions, uint8 [2, B, K, H, W]
+        if keep.dtype != torch.uint8 or tuple(keep.shape) != (2, B, K, H, W) or \
+                not keep.is_contiguous() or keep.device != noisy.device:
+            raise ValueError(f"keep must be a contiguous uint8 {(2, B, K, H, W)} on {noisy.device}")
     with _on(noisy.device):
-        st = load_library().gbm3d_stage1_denoise(
-            ctypes.c_void_p(noisy.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()),
-            ctypes.c_void_p(n_valid.data_ptr()), K, ctypes.c_void_p(sig.data_ptr()), levels,
-            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), need,
-            _stream_handle(noisy.device))
+        args = [ctypes.c_void_p(noisy.data_ptr()), B, H, W, patch, ctypes.c_void_p(idx.data_ptr()),
+                ctypes.c_void_p(n_valid.data_ptr()), K, ctypes.c_void_p(sig.data_ptr()), levels,
+                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()), need]
+        if keep is None:
+            st = load_library().gbm3d_stage1_denoise(*args, _stream_handle(noisy.device))
+        else:
+            st = load_library().gbm3d_stage1_denoise_keep(*args, ctypes.c_void_p(keep.data_ptr()),
+                                                          _stream_handle(noisy.device))
     if st != 0:
         raise GBM3DError(st, "stage1_denoise")
     return out

@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(FTHREADS) s1_syn_xy_kernel(const float* __rest
 // along z at every (b, y, x): Haar cascade (lz levels), hard threshold, inverse cascade
 template <int K>
 __global__ void __launch_bounds__(TPB) s1_z_kernel(float* __restrict__ C, int H, int W, int L, int lz,
-                                                   const float* __restrict__ sigmas) {
+                                                   const float* __restrict__ sigmas,
+                                                   uint8_t* __restrict__ keep_out) {
     const int x = blockIdx.x * TPB + threadIdx.x, y = blockIdx.y, b = blockIdx.z;
     if (x >= W) return;
     const int64_t plane = (int64_t)H * W;
@@ -469,6 +470,8 @@ __global__ void __launch_bounds__(TPB) s1_z_kernel(float* __restrict__ C, int H,
     for (int k = 0; k < K; ++k) {
         const bool keep = fabsf(v[k]) >= lam || (ll && (k % zstep) == 0);
         v[k] = keep ? v[k] : 0.f;
+        // test hook (gbm3d_stage1_denoise_keep): Upsilon's decision per coefficient
+        if (keep_out) keep_out[((int64_t)b * K + k) * plane + (int64_t)y * W + x] = keep ? 1 : 0;
     }
 #pragma unroll
     for (int t = 4; t >= 0; --t) {
@@ -621,10 +624,9 @@ extern "C" size_t gbm3d_stage1_workspace_bytes(int B, int H, int W, int patch, i
     return (3 * vol + 2 * (size_t)B * H * W) * sizeof(float);
 }
 
-extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch,
-                                    const int32_t* idx, const int32_t* n_valid, int K,
-                                    const float* sigmas, int levels, float* out, void* workspace,
-                                    size_t workspace_bytes, void* stream) {
+static int stage1_run(const int16_t* noisy, int B, int H, int W, int patch, const int32_t* idx,
+                      const int32_t* n_valid, int K, const float* sigmas, int levels, float* out,
+                      void* workspace, size_t workspace_bytes, void* stream, uint8_t* keep) {
     if (!noisy || !idx || !n_valid || !sigmas || !out || !workspace) return GBM3D_ERR_ARG;
     if (B < 1 || patch < 1 || K < 1 || levels < 1 || H < patch || W < patch) return GBM3D_ERR_ARG;
     if (H % patch || W % patch || H % (2 << levels) || W % (2 << levels)) return GBM3D_ERR_ARG;
@@ -663,13 +665,14 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
                                                                 patch, lld, ll_row0, C, K, H, W, h, w, 0);
         }
         const dim3 zg(gx, H, B);
+        uint8_t* const kp = keep ? keep + sh * vol : nullptr;
         switch (K) {
-            case 1: s1_z_kernel<1><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
-            case 2: s1_z_kernel<2><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
-            case 4: s1_z_kernel<4><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
-            case 8: s1_z_kernel<8><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
-            case 16: s1_z_kernel<16><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
-            default: s1_z_kernel<32><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas); break;
+            case 1: s1_z_kernel<1><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
+            case 2: s1_z_kernel<2><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
+            case 4: s1_z_kernel<4><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
+            case 8: s1_z_kernel<8><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
+            case 16: s1_z_kernel<16><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
+            default: s1_z_kernel<32><<<zg, TPB, 0, s>>>(C, H, W, levels, lz, sigmas, kp); break;
         }
         // synthesis: LL_l from C's corner (l = L) or the scratch offset of level l, LL_(l-1) to
         // the scratch offset of level l - 1, level 1 accumulated unshifted into U
@@ -704,4 +707,22 @@ extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, i
             s1_divide_kernel<0><<<dg, 256, 0, s>>>(num, wmap, out, H, W, patch);
     }
     return cudaGetLastError() == cudaSuccess ? GBM3D_OK : GBM3D_ERR_CUDA;
+}
+
+extern "C" int gbm3d_stage1_denoise(const int16_t* noisy, int B, int H, int W, int patch,
+                                    const int32_t* idx, const int32_t* n_valid, int K,
+                                    const float* sigmas, int levels, float* out, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    return stage1_run(noisy, B, H, W, patch, idx, n_valid, K, sigmas, levels, out, workspace,
+                      workspace_bytes, stream, nullptr);
+}
+
+extern "C" int gbm3d_stage1_denoise_keep(const int16_t* noisy, int B, int H, int W, int patch,
+                                         const int32_t* idx, const int32_t* n_valid, int K,
+                                         const float* sigmas, int levels, float* out,
+                                         void* workspace, size_t workspace_bytes,
+                                         uint8_t* keep, void* stream) {
+    if (!keep) return GBM3D_ERR_ARG;
+    return stage1_run(noisy, B, H, W, patch, idx, n_valid, K, sigmas, levels, out, workspace,
+                      workspace_bytes, stream, keep);
 }

@@ -108,3 +108,48 @@ def test_stage1_full_size_identity():
     out = g.stage1_denoise(z, idx, nv, 8, 0.0)
     torch.cuda.synchronize()
     np.testing.assert_allclose(out.cpu().numpy(), img.astype(np.float64), atol=1e-2, rtol=0)
+
+
+def test_stage1_full_size_decision_aware():
+    """BASELINE c3's full size (2048^2, tiling N8, K16, the image's sigma = 25), element-wise
+    against the float64 oracle with no allowance for flipped pixels.  Upsilon's keep / zero
+    decision flips for coefficients within rounding of lambda; the GPU exports its decisions
+    (gbm3d_stage1_denoise_keep) and (i) they must equal the oracle's for every coefficient
+    farther than 1e-3 (relative) from its threshold, (ii) the oracle then takes the GPU's
+    decision on the few within 1e-3 and every pixel must agree within 1e-2 (reading S6)."""
+    from synth import CONFIGS, config_images
+    g = _g()
+    cfg = CONFIGS["c3"]
+    img = config_images("c3")[0]
+    N, K, r, L = 8, 16, 16, 3
+    sigma = float(cfg.sigma)
+    z = torch.from_numpy(img).cuda()
+    idx, dist, nv = g.block_match(z, N, N, r, K, None)
+    keep = torch.empty((2, 1, K, cfg.H, cfg.W), dtype=torch.uint8, device="cuda")
+    out = g.stage1_denoise(z, idx, nv, N, sigma, L, keep=keep)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    gkeep = keep.cpu().numpy()[:, 0].astype(bool)
+    idx_h, nv_h = idx.cpu().numpy(), nv.cpu().numpy()
+    del keep, out
+    V = oracle.gather_volume(img, idx_h, N).astype(np.float64)
+    lev = stage1.spatial_level_map(cfg.H, cfg.W, L)
+    lam = sigma * (3.6 - 0.3 * lev)
+    hL, wL = cfg.H >> L, cfg.W >> L
+    overrides = []
+    n_amb = 0
+    for spin, h in enumerate((0, 1)):
+        T = stage1.spin_coefficients(V, h, L)
+        rel = np.abs(np.abs(T) - lam[None]) / lam[None]
+        okeep = np.abs(T) >= lam[None]
+        okeep[::8, :hL, :wL] = True           # LL_L x z-approximation (lz = 3 for K = 16)
+        rel[::8, :hL, :wL] = np.inf
+        amb = rel < 1e-3
+        n_amb += int(amb.sum())
+        mism = (gkeep[spin] != okeep) & ~amb
+        assert not mism.any(), f"spin {h}: {int(mism.sum())} decisions differ away from lambda"
+        overrides.append((amb, gkeep[spin]))
+        del T, rel, okeep
+    exp = stage1.stage1(img, idx_h, nv_h, N, sigma, L, overrides=overrides)
+    diff = np.abs(got - exp)
+    assert diff.max() < 1e-2, (float(diff.max()), n_amb)
