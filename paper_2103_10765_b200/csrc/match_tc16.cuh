@@ -72,9 +72,12 @@ constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, PRO_WARP0 = 9, NPRO_MA
 // lane quarter 0's A rows go through a small shared buffer that the MMA warp copies in.  For
 // K = 32 the second epilogue warp costs the selector more issue slots than it saves (measured,
 // DESIGN.md).
+#ifndef GBM3D_TC16_EH31
+#define GBM3D_TC16_EH31 1  // dev switch: epilogue warps per lane quarter for K = 32
+#endif
 template <int KL>
 struct Tc16Cfg {
-    static constexpr int EH = KL <= 15 ? 2 : 1;          // epilogue warps per lane quarter
+    static constexpr int EH = KL <= 15 ? 2 : GBM3D_TC16_EH31;  // epilogue warps per lane quarter
     static constexpr int NPRO = EH == 2 ? 3 : 4;         // producer warps
     static constexpr int EPI_WARP1 = PRO_WARP0 + NPRO;   // first warp of epilogue half 1
     static constexpr int THREADS = 32 * (EPI_WARP1 + (EH == 2 ? EPI_WARPS : 0));
@@ -89,6 +92,7 @@ constexpr int INFO_W = 8;        // words per entry: tile (-1 = no more), image,
 constexpr int NSCHED = 64;       // tile-counter slots (concurrent launches use different slots)
 constexpr int PRO_BAR = 2;       // named barrier of the producer warps
 constexpr int MMA_PRO_BAR = 3;   // MMA warp -> producers: the tile's MMAs completed (X, A free)
+constexpr int EPI_PRO_BAR = 4;   // [2] epilogue -> producers: the epilogue left a tile (by parity)
 #ifndef GBM3D_TC16_BULK_MIN
 #define GBM3D_TC16_BULK_MIN 16
 #endif
@@ -312,7 +316,6 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
     uint64_t* const b_xa = b_raw + 1;                    // X and A of the tile built
     uint64_t* const b_mma = b_raw + 2;                   // the tile's MMAs completed
     uint64_t* const b_nc = b_raw + 3;                    // [2] candidate norms built (by tile parity)
-    uint64_t* const b_epi = b_raw + 5;                   // [2] epilogue left the tile (by tile parity)
     uint64_t* const info_full = b_raw + 7;
     uint64_t* const info_empty = info_full + NINFO;
     volatile int* const gate_pub = reinterpret_cast<volatile int*>(info_empty + NINFO);
@@ -336,7 +339,6 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
         tc::mbar_init(b_mma, 1);
         for (int i = 0; i < 2; ++i) {
             tc::mbar_init(&b_nc[i], NPRO);
-            tc::mbar_init(&b_epi[i], EPI_WARPS * EPI_HALVES);
         }
         for (int i = 0; i < NINFO; ++i) {
             tc::mbar_init(&info_full[i], 1);
@@ -367,6 +369,8 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                     info[slot * INFO_W] = -1;
                     tc::mbar_arrive(&info_full[slot]);
                 }
+                for (int j = max(0, it - 2); j < it; ++j)  // the epilogue's last two arrivals
+                    tc::named_bar(EPI_PRO_BAR + (j & 1), 32 * (NPRO + EPI_WARPS * EPI_HALVES));
                 break;
             }
             const Tc16Tile T(p, tile);
@@ -485,7 +489,9 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
             // (4) candidate norms N_q = P x P box sums of squares (integers < 2^24: exact in
             // fp32) into the buffer of this tile's parity, free once the epilogue left tile it - 2
             // (long ago: built during the previous tile); a thread per (column, half)
-            if (it > 1) tc::mbar_wait_long(&b_epi[it & 1], ((it >> 1) - 1) & 1, 512);
+            // (a named barrier per tile parity: the producers sleep in hardware; the epilogue
+            // cannot leave tile it before these norms exist, so the arrivals alternate)
+            if (it > 1) tc::named_bar(EPI_PRO_BAR + (it & 1), 32 * (NPRO + EPI_WARPS * EPI_HALVES));
             float* const nc = nc2 + (it & 1) * g.NT * NB;
             if (tr) TC_TRP(2000 + it * 8 + 6, clock64());
             for (int task = tp; !skip && task < 2 * NB; task += 32 * NPRO) {
@@ -705,6 +711,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                             gate = gate_pub[w * 32 + lane];
                         }
                     }
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6600 + (used - tile_start), clock64());
                     const float Tg = (float)(gate - __float2int_rn(Nr));
                     uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
                     tc::tc_fence_after();
@@ -716,6 +723,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                     tc::tmem_wait_ld();
 #pragma unroll
                     for (int ch = 0; ch < 4; ++ch) tc::tmem_tie16(acc + ch * 16);
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6900 + (used - tile_start), clock64());
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
                         const int ch = cc ^ 1;  // per 32-column half, the upper 16 columns first
@@ -737,6 +745,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                             *reinterpret_cast<float4*>(stg + ch * 16 + 4 * q) =
                                 make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                     }
+                    if (lane == 0 && it == 5 && w == 0) TC_TRP(7000 + (used - tile_start), clock64());
                     tc::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&tempty[ts]);
@@ -753,7 +762,9 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&b_epi[it & 1]);  // nc buffer (it & 1) free again
+            // nc buffer (it & 1) free again
+            asm volatile("bar.arrive %0, %1;" ::"r"(EPI_PRO_BAR + (it & 1)),
+                         "r"(32 * (NPRO + EPI_WARPS * EPI_HALVES)) : "memory");
             if (lane == 0 && it < 40) TC_TRP(4000 + it * 16 + w * 4 + 2, clock64());
         }
     } else if (warp >= SEL_WARP0 && warp < SEL_WARP0 + EPI_WARPS) {
