@@ -140,15 +140,43 @@ def _check_cuda_int16(t, name):
         raise ValueError(f"{name} must be contiguous")
 
 
+# Range checks that passed, per live tensor object: (weakref, version counter, data_ptr, numel)
+# -> largest patch that passed (the bound P^2 (max-min)^2 <= 2^31-1 then holds for every smaller
+# patch).  A tensor modified in place bumps its version counter, so a stale entry never matches.
+_range_ok = {}
+
+
+def _range_cached(img, patch: int) -> bool:
+    e = _range_ok.get(id(img))
+    return (e is not None and e[0]() is img and e[1] == img._version and e[2] == img.data_ptr()
+            and e[3] == img.numel() and patch <= e[4])
+
+
+def _range_remember(img, patch: int):
+    import weakref
+    if len(_range_ok) > 256:
+        for k in [k for k, e in _range_ok.items() if e[0]() is None]:
+            del _range_ok[k]
+        if len(_range_ok) > 256:
+            _range_ok.clear()
+    _range_ok[id(img)] = (weakref.ref(img), img._version, img.data_ptr(), img.numel(), patch)
+
+
 def check_range(img, patch: int) -> bool:
-    """P^2 (max-min)^2 <= 2^31-1 on the device (reading R10).  Synchronises the stream."""
+    """P^2 (max-min)^2 <= 2^31-1 on the device (reading R10).  Synchronises the stream, except
+    when this same tensor object, unmodified since (same version counter), already passed for a
+    patch at least as large."""
     _check_cuda_int16(img, "img")
+    if _range_cached(img, patch):
+        return True
     ok = ctypes.c_int(0)
     with _on(img.device):
         st = load_library().gbm3d_check_range(ctypes.c_void_p(img.data_ptr()), img.numel(), patch,
                                               ctypes.byref(ok), _stream_handle(img.device))
     if st != 0:
         raise GBM3DError(st, "check_range")
+    if ok.value:
+        _range_remember(img, patch)
     return bool(ok.value)
 
 
@@ -176,7 +204,9 @@ def block_match(img, patch: int, stride: int, radius: int, K: int, tau: Optional
     [(B,) Ry, Rx]: slot 0 = the reference (d = 0), slots 1..n_valid-1 = the K-1 nearest
     candidates of the clamped (2 radius + 1)^2 window by (SSD, raster index) with SSD < tau,
     pads = (reference, -1).  Enqueued on torch's current stream.  ``check`` runs the
-    (blocking) range precondition first."""
+    range precondition first (``check_range``: a stream synchronisation, skipped for a tensor
+    that already passed and was not modified since); callers that know their pixel range pass
+    ``check=False`` for a fully asynchronous call."""
     _check_cuda_int16(img, "img")
     batched = img.dim() == 3
     if img.dim() not in (2, 3):

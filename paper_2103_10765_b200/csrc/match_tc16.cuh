@@ -289,6 +289,145 @@ struct Tc16Tile {
     }
 };
 
+// Insert one staged row's passing candidates into the lane's sorted list L: dense rows (R =
+// max pass count over the warp >= BULK_MIN) by bitonic sort + merge of the window columns
+// j0 .. j0 + 39, the rest by insertion rounds of two keys (list_insert2).  stg = the lane's
+// staged v values (d = v + gate), GB = gate + 2^23 as fp32: bits(v + GB) = 0x4B000000 + d, whose
+// 0x4B000000 part vanishes in the shift by cb >= 8.  
+template <int KP>
+static __device__ __forceinline__ void tc16_insert_row(uint32_t (&L)[KP], const uint32_t* stg,
+                                                       uint32_t mlo, uint32_t mhi, float GB,
+                                                       uint32_t code_row, uint32_t kmul, int j0,
+                                                       int r, int R) {
+    if (R >= tc16::BULK_MIN) {
+        // dense row (lists filling): window columns j0 .. j0 + 31 by sort + merge,
+        // the rest (if any) by the insertion rounds below
+        const uint64_t mw = ((((uint64_t)mhi) << 32) | mlo) >> j0;
+#pragma unroll
+        for (int c = 0; c < 32 / KP; ++c) {
+            uint32_t B[KP];
+#pragma unroll
+            for (int jj = 0; jj < KP; ++jj) {
+                const int col = c * KP + jj;
+                const uint32_t bits =
+                    __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
+                B[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
+                                             : KEY_INF;
+            }
+            bulk_merge<KP>(L, B);
+        }
+        uint64_t rest = ((((uint64_t)mhi) << 32) | mlo) & ~(0xffffffffull << j0);
+        if (2 * r + 1 <= 40) {  // the (at most 8) window columns left: one more batch
+            uint32_t B8[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int col = 32 + jj;
+                const uint32_t bits =
+                    __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
+                B8[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
+                                              : KEY_INF;
+            }
+            bulk_merge8<KP>(L, B8);
+            rest = 0ull;
+        }
+        mlo = (uint32_t)rest;
+        mhi = (uint32_t)(rest >> 32);
+        R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
+    }
+    // next pending candidate (highest column first), software-pipelined one round
+    // ahead of the insertion network
+    auto next_key = [&]() -> uint32_t {
+        const bool hi = mhi != 0u;
+        const uint32_t m = hi ? mhi : mlo;
+        const int jb = 31 - __clz(m);  // -1 when nothing is pending
+        const int j = (hi ? 32 : 0) + max(jb, 0);
+        const uint32_t clr = m ^ (jb >= 0 ? (1u << jb) : 0u);
+        if (hi) mhi = clr; else mlo = clr;
+        const uint32_t bits = __float_as_uint(__uint_as_float(stg[j]) + GB);
+        return jb >= 0 ? bits * kmul + code_row + (uint32_t)j : KEY_INF;
+    };
+    // two pending keys per round (the second is KEY_INF when a lane has run out)
+    uint32_t ka = next_key(), kb = next_key();
+    for (int q = 0; q < (R + 1) >> 1; ++q) {
+        const uint32_t ca = ka, cb2 = kb;
+        ka = next_key();
+        kb = next_key();
+        list_insert2<KP>(L, ca, cb2);
+    }
+}
+
+// A lane's reference after its tile: slot 0 = self, ranks 1.. = the list (keys decoded to image
+// indices and distances), pads; n_valid; the exact 64-bit recompute when tau exceeds the key
+// range and the list did not fill.
+template <int S, int KL>
+static __device__ __forceinline__ void tc16_write_refs(const MatchParams& p, const uint32_t (&L)[KL + 1],
+                                                       int a, int bb, int ky0, int kx0, int bimg,
+                                                       int cb, uint32_t side) {
+    constexpr int P = 8;
+    const int r = p.r;
+    const int Kout = p.K;
+    const int ry = S * (ky0 + a), rx = S * (kx0 + bb);
+    const int self = ry * p.W + rx;
+    const uint32_t cmask = (1u << cb) - 1u;
+    // idx = self + dy W + dx with code = (dy + r) side + (dx + r): with q = code / side
+    // (exact through the fp32 reciprocal: code < 2^13, side <= 65),
+    // idx = self - r (W + 1) + code + q (W - side)
+    const float inv_side = 1.0f / (float)side;
+    const int ibase = self - r * (p.W + 1), wms = p.W - (int)side;
+    auto slot_val = [&](int i, int32_t& vi, int32_t& vd) {  // i = slot (static)
+        vi = self;
+        vd = i == 0 ? 0 : -1;
+        if (i > 0) {
+            const uint32_t key = L[i - 1];
+            if (key != KEY_INF) {
+                const uint32_t code = key & cmask;
+                const int q = (int)(((float)code + 0.5f) * inv_side);
+                vi = ibase + (int)code + q * wms;
+                vd = (int32_t)(key >> cb);
+            }
+        }
+    };
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) cnt += (i + 1 < Kout && L[i] != KEY_INF) ? 1 : 0;
+    const int64_t ref = (int64_t)bimg * p.out_bstride +
+                        (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
+    int32_t* const oi = p.idx + ref * Kout;
+    int32_t* const od = p.dist + ref * Kout;
+    if ((Kout & 3) == 0) {
+#pragma unroll
+        for (int c = 0; c < (KL + 1) / 4; ++c) {
+            if (4 * c < Kout) {
+                int32_t i0, i1, i2, i3, d0, d1, d2, d3;
+                slot_val(4 * c + 0, i0, d0);
+                slot_val(4 * c + 1, i1, d1);
+                slot_val(4 * c + 2, i2, d2);
+                slot_val(4 * c + 3, i3, d3);
+                *reinterpret_cast<int4*>(oi + 4 * c) = make_int4(i0, i1, i2, i3);
+                *reinterpret_cast<int4*>(od + 4 * c) = make_int4(d0, d1, d2, d3);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < KL + 1; ++i) {
+            if (i < Kout) {
+                int32_t vi, vd;
+                slot_val(i, vi, vd);
+                oi[i] = vi;
+                od[i] = vd;
+            }
+        }
+    }
+    if (p.tau_above_dsat && cnt < Kout - 1) {
+        const int wy = min(p.H - P, ry + r) - max(0, ry - r) + 1;
+        const int wx = min(p.W - P, rx + r) - max(0, rx - r) + 1;
+        if (cnt < wy * wx - 1)
+            cnt = tc_exact_ref(p.img + (int64_t)bimg * p.img_bstride, p.slab_y0, p.H,
+                               p.W, P, r, ry, rx, Kout, p.tau, oi, od);
+    }
+    if (p.nvalid) p.nvalid[ref] = 1 + cnt;
+}
+
 template <int S, int KL>
 __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
     match_tc16_kernel(MatchParams p, const __grid_constant__ CUtensorMap tmap, int use_tma, int ntiles,
@@ -815,62 +954,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                 const float GB = (float)(int)hdr.z + 8388608.0f;  // d + 2^23 = v + gate + 2^23
                 const uint32_t code_row = (uint32_t)((int)hdr.w - S * a) * side - (uint32_t)(S * bb);
                 int R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
-                if (R >= BULK_MIN) {
-                    // dense row (lists filling): window columns j0 .. j0 + 31 by sort + merge,
-                    // the rest (if any) by the insertion rounds below
-                    const int j0 = S * bb;
-                    const uint64_t mw = ((((uint64_t)mhi) << 32) | mlo) >> j0;
-#pragma unroll
-                    for (int c = 0; c < 32 / KP; ++c) {
-                        uint32_t B[KP];
-#pragma unroll
-                        for (int jj = 0; jj < KP; ++jj) {
-                            const int col = c * KP + jj;
-                            const uint32_t bits =
-                                __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
-                            B[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
-                                                         : KEY_INF;
-                        }
-                        bulk_merge<KP>(L, B);
-                    }
-                    uint64_t rest = ((((uint64_t)mhi) << 32) | mlo) & ~(0xffffffffull << j0);
-                    if (2 * r + 1 <= 40) {  // the (at most 8) window columns left: one more batch
-                        uint32_t B8[8];
-#pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) {
-                            const int col = 32 + jj;
-                            const uint32_t bits =
-                                __float_as_uint(__uint_as_float(stg[j0 + col]) + GB);
-                            B8[jj] = ((mw >> col) & 1ull) ? bits * kmul + code_row + (uint32_t)(j0 + col)
-                                                          : KEY_INF;
-                        }
-                        bulk_merge8<KP>(L, B8);
-                        rest = 0ull;
-                    }
-                    mlo = (uint32_t)rest;
-                    mhi = (uint32_t)(rest >> 32);
-                    R = (int)__reduce_max_sync(0xffffffffu, (unsigned)(__popc(mlo) + __popc(mhi)));
-                }
-                // next pending candidate (highest column first), software-pipelined one round
-                // ahead of the insertion network
-                auto next_key = [&]() -> uint32_t {
-                    const bool hi = mhi != 0u;
-                    const uint32_t m = hi ? mhi : mlo;
-                    const int jb = 31 - __clz(m);  // -1 when nothing is pending
-                    const int j = (hi ? 32 : 0) + max(jb, 0);
-                    const uint32_t clr = m ^ (jb >= 0 ? (1u << jb) : 0u);
-                    if (hi) mhi = clr; else mlo = clr;
-                    const uint32_t bits = __float_as_uint(__uint_as_float(stg[j]) + GB);
-                    return jb >= 0 ? bits * kmul + code_row + (uint32_t)j : KEY_INF;
-                };
-                // two pending keys per round (the second is KEY_INF when a lane has run out)
-                uint32_t ka = next_key(), kb = next_key();
-                for (int q = 0; q < (R + 1) >> 1; ++q) {
-                    const uint32_t ca = ka, cb2 = kb;
-                    ka = next_key();
-                    kb = next_key();
-                    list_insert2<KP>(L, ca, cb2);
-                }
+                tc16_insert_row<KP>(L, stg, mlo, mhi, GB, code_row, kmul, S * bb, r, R);
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sempty[w * NSLOT + slot]);
                 const uint32_t top = L[KL - 1];
@@ -885,69 +969,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
             }
             if (lane == 0 && it < 40) TC_TRP(5000 + it * 16 + w * 4 + 2, clock64());
             // ---- output straight from the registers: slot 0 = self, ranks 1.. = list, pads
-            if (refok) {
-                const int Kout = p.K;
-                const int ry = S * (ky0 + a), rx = S * (kx0 + bb);
-                const int self = ry * p.W + rx;
-                const uint32_t cmask = (1u << cb) - 1u;
-                // idx = self + dy W + dx with code = (dy + r) side + (dx + r): with q = code / side
-                // (exact through the fp32 reciprocal: code < 2^13, side <= 65),
-                // idx = self - r (W + 1) + code + q (W - side)
-                const float inv_side = 1.0f / (float)side;
-                const int ibase = self - r * (p.W + 1), wms = p.W - (int)side;
-                auto slot_val = [&](int i, int32_t& vi, int32_t& vd) {  // i = slot (static)
-                    vi = self;
-                    vd = i == 0 ? 0 : -1;
-                    if (i > 0) {
-                        const uint32_t key = L[i - 1];
-                        if (key != KEY_INF) {
-                            const uint32_t code = key & cmask;
-                            const int q = (int)(((float)code + 0.5f) * inv_side);
-                            vi = ibase + (int)code + q * wms;
-                            vd = (int32_t)(key >> cb);
-                        }
-                    }
-                };
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < KL; ++i) cnt += (i + 1 < Kout && L[i] != KEY_INF) ? 1 : 0;
-                const int64_t ref = (int64_t)bimg * p.out_bstride +
-                                    (int64_t)(ky0 + a - p.row_begin) * p.Rx + (kx0 + bb);
-                int32_t* const oi = p.idx + ref * Kout;
-                int32_t* const od = p.dist + ref * Kout;
-                if ((Kout & 3) == 0) {
-#pragma unroll
-                    for (int c = 0; c < (KL + 1) / 4; ++c) {
-                        if (4 * c < Kout) {
-                            int32_t i0, i1, i2, i3, d0, d1, d2, d3;
-                            slot_val(4 * c + 0, i0, d0);
-                            slot_val(4 * c + 1, i1, d1);
-                            slot_val(4 * c + 2, i2, d2);
-                            slot_val(4 * c + 3, i3, d3);
-                            *reinterpret_cast<int4*>(oi + 4 * c) = make_int4(i0, i1, i2, i3);
-                            *reinterpret_cast<int4*>(od + 4 * c) = make_int4(d0, d1, d2, d3);
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < KL + 1; ++i) {
-                        if (i < Kout) {
-                            int32_t vi, vd;
-                            slot_val(i, vi, vd);
-                            oi[i] = vi;
-                            od[i] = vd;
-                        }
-                    }
-                }
-                if (p.tau_above_dsat && cnt < Kout - 1) {
-                    const int wy = min(p.H - P, ry + r) - max(0, ry - r) + 1;
-                    const int wx = min(p.W - P, rx + r) - max(0, rx - r) + 1;
-                    if (cnt < wy * wx - 1)
-                        cnt = tc_exact_ref(p.img + (int64_t)bimg * p.img_bstride, p.slab_y0, p.H,
-                                           p.W, P, r, ry, rx, Kout, p.tau, oi, od);
-                }
-                if (p.nvalid) p.nvalid[ref] = 1 + cnt;
-            }
+            if (refok) tc16_write_refs<S, KL>(p, L, a, bb, ky0, kx0, bimg, cb, side);
             __syncwarp();
             if (lane == 0 && it < 40) TC_TRP(5000 + it * 16 + w * 4 + 3, clock64());
         }

@@ -276,6 +276,25 @@ def test_check_range_and_error_codes():
         g.block_match(ok, 17, 3, 19, 16)          # patch > 16 -> UNSUPPORTED
 
 
+def test_check_range_cache_follows_modifications():
+    """A passed range check is remembered per tensor object and version counter: an in-place
+    write that breaks the bound is caught again, a larger patch is re-checked."""
+    g = _gbm3d()
+    img = torch.zeros((16, 16), dtype=torch.int16, device="cuda")
+    img[0, 0] = 5000
+    assert g.check_range(img, 8)                  # 64 * 5000^2 < 2^31
+    assert g._range_cached(img, 8) and g._range_cached(img, 4)
+    assert not g._range_cached(img, 12)           # a larger patch is checked again
+    assert not g.check_range(img, 12)             # 144 * 5000^2 > 2^31
+    img[1, 1] = -5000                             # in place: version counter bumps
+    assert not g._range_cached(img, 8)
+    assert not g.check_range(img, 8)              # 64 * 10000^2 > 2^31
+    with pytest.raises(g.GBM3DError):
+        g.block_match(img, 8, 3, 4, 4)
+    other = img.clone()
+    assert not g._range_cached(other, 2)          # another tensor object: no entry
+
+
 def test_deterministic_repeat():
     img = torch.from_numpy(config_images("c2")[0]).cuda()
     g = _gbm3d()
