@@ -284,8 +284,12 @@ static __device__ __noinline__ int strip_exact_ref(const int16_t* __restrict__ s
 // nsplit > 1 (small images): the CTAs of a cluster of nsplit along z share one strip tile and
 // take interleaved subsets of the displacement blocks; cluster rank 0 merges the others' sorted
 // heaps through distributed shared memory and writes the tables (more CTAs fill the GPU).
+#ifndef GBM3D_S12_MINB
+#define GBM3D_S12_MINB 3  // patch-12 shape: 3 resident CTAs per SM (168 registers; c2 0.31 -> 0.28 ms)
+#endif
 template <class Cfg>
-__global__ void __launch_bounds__(128) match_strip_kernel(MatchParams p, int NS, int nsplit) {
+__global__ void __launch_bounds__(128, Cfg::P == 12 ? GBM3D_S12_MINB : 1)
+    match_strip_kernel(MatchParams p, int NS, int nsplit) {
     constexpr int S = Cfg::S, P = Cfg::P, D = Cfg::D, NR = Cfg::NR, TRY = Cfg::TRY;
     constexpr int RC = Cfg::RC, CB = Cfg::CB, WPS = Cfg::WPS, HALF = TRY / WPS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -639,10 +643,18 @@ cudaError_t launch_strip(const MatchParams& p, cudaStream_t stream, int* launche
     const long long cap = (long long)n_sm * (best_warps / (Cfg::WPS * best_ns));
     int nsplit = 1;
     if (!p.tau_above_dsat && p.K - 1 <= Cfg::TRY * Cfg::D && ctas < cap) {
-        // about 1.5 waves of the resident CTA slots (measured on c2: 1.5 -> 3 splits, 0.38 ->
-        // 0.31 ms; 2 / 4 / 6 / 8 splits 0.33 / 0.34 / 0.40 / 0.47 ms)
-        nsplit = (int)((3 * cap + 2 * ctas - 1) / (2 * ctas));
-        nsplit = nsplit > 4 ? 4 : nsplit;
+        // the split (<= 4) whose CTAs fill their waves of resident slots best, ties to fewer
+        // splits (c2 measured, 3 CTAs/SM = 444 slots for 160 CTAs: 1 / 2 / 3 / 4 splits 0.406 /
+        // 0.283 / 0.331 / 0.314 ms -> 2; at 2 CTAs/SM (296 slots) 3 splits won, 0.309 ms)
+        double best = 0.0;
+        for (int ns = 1; ns <= 4; ++ns) {
+            const long long n = ctas * ns, waves = (n + cap - 1) / cap;
+            const double eff = (double)n / (double)(waves * cap);
+            if (eff > best + 1e-9) {
+                best = eff;
+                nsplit = ns;
+            }
+        }
     }
     static const int split_env = getenv("GBM3D_STRIP_SPLIT") ? atoi(getenv("GBM3D_STRIP_SPLIT")) : 0;
     if (split_env > 0 && !p.tau_above_dsat && p.K - 1 <= Cfg::TRY * Cfg::D) nsplit = split_env;  // dev
