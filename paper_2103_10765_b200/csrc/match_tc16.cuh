@@ -72,6 +72,16 @@ constexpr int EPI_WARPS = 4, SEL_WARP0 = 4, MMA_WARP = 8, PRO_WARP0 = 9, NPRO_MA
 // lane quarter 0's A rows go through a small shared buffer that the MMA warp copies in.  For
 // K = 32 the second epilogue warp costs the selector more issue slots than it saves (measured,
 // DESIGN.md).
+#ifndef GBM3D_TC16_EARLY15
+#define GBM3D_TC16_EARLY15 1  // K <= 16: u and the TMEM release before the slot / gate wait
+#endif
+#ifndef GBM3D_TC16_GATEFLAG15
+#define GBM3D_TC16_GATEFLAG15 1  // K <= 16: no vote once the quarter's lists are full
+#endif
+#ifndef GBM3D_TC16_BULK_MIN15
+#define GBM3D_TC16_BULK_MIN15 20
+#endif
+constexpr bool EARLY15 = GBM3D_TC16_EARLY15, GATEFLAG15 = GBM3D_TC16_GATEFLAG15;
 #ifndef GBM3D_TC16_EH31
 #define GBM3D_TC16_EH31 1  // dev switch: epilogue warps per lane quarter for K = 32
 #endif
@@ -299,7 +309,7 @@ static __device__ __forceinline__ void tc16_insert_row(uint32_t (&L)[KP], const 
                                                        uint32_t mlo, uint32_t mhi, float GB,
                                                        uint32_t code_row, uint32_t kmul, int j0,
                                                        int r, int R) {
-    if (R >= tc16::BULK_MIN) {
+    if (R >= (KP <= 16 ? GBM3D_TC16_BULK_MIN15 : tc16::BULK_MIN)) {
         // dense row (lists filling): window columns j0 .. j0 + 31 by sort + merge,
         // the rest (if any) by the insertion rounds below
         const uint64_t mw = ((((uint64_t)mhi) << 32) | mlo) >> j0;
@@ -819,6 +829,7 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
             if (!skip) {
                 const float Nr = nc[ty * NB + tx];
                 const int tile_start = used;
+                bool lists_full = false;
                 if (lane == 0 && it < 40) TC_TRP(4400 + it * 8 + w, clock64());
                 const int nseq = t_hi - t_lo + 1;
                 for (int k = 0; k < nseq; ++k, ++s) {
@@ -840,41 +851,79 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                         ++used;
                         continue;
                     }
+                    // EARLY (two epilogue halves): the gate-independent half first -- TMEM
+                    // load, u = N_q - 2 <f_p, f_q>, TMEM stage released -- then the staging slot
+                    // and the gate; otherwise v = u - T in one pass after the gate is known
+                    constexpr bool EARLY = EPI_HALVES == 2 && EARLY15;
+                    const uint32_t tb = taddr + (uint32_t)(ts * NB);
+                    uint32_t acc[64];
+                    if (EARLY) {
+                        tc::tc_fence_after();
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) tc::tmem_ld16p(tb + ch * 16, acc + ch * 16);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) tc::tmem_tie16(acc + ch * 16);
+                        tc::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                        const float4* ncv = reinterpret_cast<const float4*>(nc + t * NB);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            const float4 n4 = ncv[q];
+                            uint32_t* const u = acc + 4 * q;
+                            u[0] = __float_as_uint(fmaf(__uint_as_float(u[0]), -2.f, n4.x));
+                            u[1] = __float_as_uint(fmaf(__uint_as_float(u[1]), -2.f, n4.y));
+                            u[2] = __float_as_uint(fmaf(__uint_as_float(u[2]), -2.f, n4.z));
+                            u[3] = __float_as_uint(fmaf(__uint_as_float(u[3]), -2.f, n4.w));
+                        }
+                    }
                     if (used >= NSLOT) tc::mbar_wait(&sempty[w * NSLOT + slot], ((used / NSLOT) - 1) & 1);
                     int gate = gate0;
                     if (used > tile_start) {
-                        while (consumed[w] <= tile_start) __nanosleep(32);
+                        // (once every list of the quarter is full in this tile, no more votes)
+                        const bool check = !(EPI_HALVES == 2 && GATEFLAG15 && lists_full);
+                        if (check) while (consumed[w] <= tile_start) __nanosleep(32);
                         gate = gate_pub[w * 32 + lane];
-                        if (__any_sync(0xffffffffu, gate == gate0 && refok)) {
-                            while (consumed[w] < used) __nanosleep(32);
-                            gate = gate_pub[w * 32 + lane];
+                        if (check) {
+                            if (__any_sync(0xffffffffu, gate == gate0 && refok)) {
+                                while (consumed[w] < used) __nanosleep(32);
+                                gate = gate_pub[w * 32 + lane];
+                            } else {
+                                lists_full = true;
+                            }
                         }
                     }
                     if (lane == 0 && it == 5 && w == 0) TC_TRP(6600 + (used - tile_start), clock64());
                     const float Tg = (float)(gate - __float2int_rn(Nr));
                     uint32_t* const stg = stg0 + slot * 32 * STG_PITCH;
-                    tc::tc_fence_after();
                     uint32_t msk[2] = {0u, 0u};
-                    const uint32_t tb = taddr + (uint32_t)(ts * NB);
-                    uint32_t acc[64];
+                    if (!EARLY) {
+                        tc::tc_fence_after();
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) tc::tmem_ld16p(tb + ch * 16, acc + ch * 16);
-                    tc::tmem_wait_ld();
+                        for (int ch = 0; ch < 4; ++ch) tc::tmem_ld16p(tb + ch * 16, acc + ch * 16);
+                        tc::tmem_wait_ld();
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) tc::tmem_tie16(acc + ch * 16);
-                    if (lane == 0 && it == 5 && w == 0) TC_TRP(6900 + (used - tile_start), clock64());
+                        for (int ch = 0; ch < 4; ++ch) tc::tmem_tie16(acc + ch * 16);
+                        if (lane == 0 && it == 5 && w == 0) TC_TRP(6900 + (used - tile_start), clock64());
+                    }
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
                         const int ch = cc ^ 1;  // per 32-column half, the upper 16 columns first
-                        const float4* ncv = reinterpret_cast<const float4*>(nc + t * NB + ch * 16);
                         float v[16];
+                        if (EARLY) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float4 n4 = ncv[q];
-                            v[4 * q + 0] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 0]), -2.f, n4.x - Tg);
-                            v[4 * q + 1] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 1]), -2.f, n4.y - Tg);
-                            v[4 * q + 2] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 2]), -2.f, n4.z - Tg);
-                            v[4 * q + 3] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 3]), -2.f, n4.w - Tg);
+                            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(acc[16 * ch + j]) - Tg;
+                        } else {
+                            const float4* ncv = reinterpret_cast<const float4*>(nc + t * NB + ch * 16);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float4 n4 = ncv[q];
+                                v[4 * q + 0] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 0]), -2.f, n4.x - Tg);
+                                v[4 * q + 1] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 1]), -2.f, n4.y - Tg);
+                                v[4 * q + 2] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 2]), -2.f, n4.z - Tg);
+                                v[4 * q + 3] = fmaf(__uint_as_float(acc[16 * ch + 4 * q + 3]), -2.f, n4.w - Tg);
+                            }
                         }
                         uint32_t& m = msk[ch >> 1];
 #pragma unroll
@@ -885,9 +934,11 @@ __global__ void __launch_bounds__(tc16::Tc16Cfg<KL>::THREADS, 1)
                                 make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                     }
                     if (lane == 0 && it == 5 && w == 0) TC_TRP(7000 + (used - tile_start), clock64());
-                    tc::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                    if (!EARLY) {
+                        tc::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                    }
                     const bool rowin = refok && t >= S * a && t <= S * a + 2 * r;
                     uint64_t mm = rowin ? ((((uint64_t)msk[1]) << 32 | msk[0]) & cm) : 0ull;
                     if (t == ty) mm &= ~(1ull << tx);  // the reference itself is slot 0
