@@ -311,7 +311,7 @@ size_t gbm3d_host_workspace_bytes(int B, int H, int W, int patch, int stride, in
 // are created once per host thread and device (thread_local) and reused; nothing else is
 // allocated.
 namespace {
-constexpr int kMaxChunks = 16;
+constexpr int kMaxChunks = 64;
 struct HostPipe {
     cudaStream_t h2d = nullptr, d2h = nullptr, comp2 = nullptr;
     cudaEvent_t in[kMaxChunks], done[kMaxChunks], out_done, start;
