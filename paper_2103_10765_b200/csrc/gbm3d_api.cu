@@ -12,6 +12,7 @@
 #include "strip_p8s8.cuh"
 #include "strip_p12s4.cuh"
 #include "match_tc16.cuh"
+#include "match_tcp.cuh"
 
 namespace gbm3d {
 
@@ -52,9 +53,20 @@ extern template cudaError_t launch_tc<3, 15>(const MatchParams&, cudaStream_t, i
 extern template cudaError_t launch_tc<3, 31>(const MatchParams&, cudaStream_t, int*, int);
 extern template cudaError_t launch_tc16<3, 15>(const MatchParams&, cudaStream_t, int*);
 extern template cudaError_t launch_tc16<3, 31>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 15>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream_t, int*);
 static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok,
                                bool int8_only) {
     *ok = false;
+    // patch 12 / stride 4 (c2): fp16 product form with an in-kernel exact path for tiles above
+    // the fp16 bound; needs tau - 1 <= dsat (every listed key exact) and the tile's columns
+    // 7S + 2r + 1 <= 80 within the shared-memory bound (radius <= 21)
+    if (p.P == 12 && p.S == 4 && !int8_only && p.r <= tcp::MAX_R && 7 * p.S + 2 * p.r + 1 <= tcp::NB &&
+        p.K >= 2 && p.K <= 32 && !p.tau_above_dsat) {
+        *ok = true;
+        if (p.K - 1 <= 15) return launch_tcp<12, 4, 15>(p, st, launches);
+        return launch_tcp<12, 4, 31>(p, st, launches);
+    }
     if (p.P != 8 || p.S != 3 || 7 * p.S + 2 * p.r + 1 > tcm::NB || p.K < 2 || p.K > 32)
         return cudaSuccess;
     *ok = true;

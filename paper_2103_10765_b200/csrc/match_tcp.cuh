@@ -1,0 +1,477 @@
+// Product-form block matching on the tensor cores for patch 12 / stride 4 (BASELINE c2, the
+// high-noise profile of PAPER.md:250-253).
+//
+// Method.  As match_tc16.cuh: d(p, q) = ||f_p||^2 + ||f_q||^2 - 2 <f_p, f_q> (Eq. (2),
+// PAPER.md:82), the norms as box sums (step 1), the local cross-correlations
+// (Prop. 1) as tcgen05.mma kind::f16 inner products of a 128-reference tile with
+// each candidate row.  Exactness: the tile's pixels are centred on c = (min + max) / 2 and held as
+// fp16 of z - c (exact for |z - c| <= 2048); every partial sum of <f_p, f_q> is an integer of
+// magnitude <= P^2 M^2 (M = max |z - c|), exact in the fp32 accumulator while P^2 M^2 <= 2^24
+// (M <= 341 at P = 12).  A tile above the bound takes an in-kernel exact int32 path (direct
+// Eq. (1) sums from the pixel plane), so every tile is bit-exact.
+//
+// Layout.
+//   * Tile = 16 x 8 grid references = MMA M = 128 (TMEM lane m = reference 8a + b); one CTA per
+//     tile (c2's 512^2 image: 124 tiles for 148 SMs, a single wave).
+//   * The union of the tile's windows is NT = 15S + 2r + 1 candidate rows x NJ = 7S + 2r + 1
+//     (<= NB = 80) candidate columns.  One candidate row = one M128 N80 product over K = 12 patch
+//     rows x 16 (the last 4 fp16 of every patch row are zero in A): 12 MMAs of K16.
+//   * B needs no per-row building: the tile's centred fp16 plane is written once pre-shifted,
+//     X[y][q][m][e] = plane[y][8q + m + e], so candidate row t's K16 step i (patch row i) is the
+//     canonical K-major operand at X + (t + i) * XP with LBO = SBO = 128 B (next 8 pixels of the
+//     patch row / next 8 candidates).  A (the 128 reference patches) lives in tensor memory.
+//   * Warps 0-3 (one per TMEM lane quarter, lane = reference): per row, tcgen05.ld of the 80
+//     accumulators, u = N_q - 2<> (one FFMA), pass masks from the sign of u - T against the
+//     reference's gate T, u staged to shared memory, then insertion rounds of two keys per lane
+//     into a sorted register list of the K - 1 smallest 32-bit keys (d << cb | code; key order =
+//     (d, idx) order, reading R5).  Warp 4 allocates TMEM and issues the MMAs (4 accumulator
+//     stages); warps 5-7 help with the prologue only.
+//   * Candidate rows are visited in a scrambled order (t = t_lo + s * step mod n, step coprime to
+//     n near 0.618 n) so that every warp has work in every stretch of rows and the lists fill
+//     with typical distances early.
+//   * Keys are exact because the call's tau satisfies tau - 1 <= dsat (the dispatcher's
+//     condition): a candidate with d > tau - 1 never enters a list.
+#pragma once
+#include <cuda_fp16.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace gbm3d {
+namespace tcp {
+constexpr int TY = 16, TX = 8;       // reference tile (grid rows x grid cols) = 128 MMA rows
+constexpr int NB = 80;               // candidate columns per MMA (N), >= 7S + 2r + 1
+constexpr int PW = 96;               // pixel plane pitch (int16): NB + 16
+constexpr int XQ = NB / 8;           // 16-byte pixel groups per pre-shifted row
+constexpr int XP = XQ * 128;         // bytes per pre-shifted plane row (8 shifts per group)
+constexpr int NTS = 4;               // accumulator stages in flight
+constexpr int SPITCH = 96;           // TMEM columns per stage (N = 80, 32-column aligned)
+constexpr int TM_A = NTS * SPITCH;   // A operand: 12 K16 steps x 8 columns (two fp16 each)
+constexpr int EPI_WARPS = 4, MMA_WARP = 4, NWARPS = 8, THREADS = 32 * NWARPS;
+constexpr int STG_PITCH = 84;        // floats per lane and staged row (conflict-free STS.128)
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int MAX_R = 21;            // shared memory bound (see TcpGeom)
+}  // namespace tcp
+
+// Shared-memory carve-up of one CTA (host and device agree).
+struct TcpGeom {
+    int NT, NJ, PR;
+    int off_x, off_nq, off_raw, off_bar, total;
+    __host__ __device__ static TcpGeom make(int P, int S, int r) {
+        using namespace tcp;
+        TcpGeom g;
+        g.NT = 15 * S + 2 * r + 1;
+        g.NJ = 7 * S + 2 * r + 1;
+        g.PR = g.NT + P - 1;
+        g.off_x = 0;                                          // X (+ one pad row); prologue: hs
+        g.off_nq = (g.PR + 1) * XP;                           // candidate norms [NT][NB] fp32
+        g.off_raw = g.off_nq + g.NT * NB * 4;                 // int16 plane [PR][PW] / staging
+        const int raw = g.PR * PW * 2, stg = EPI_WARPS * 32 * STG_PITCH * 4;
+        g.off_bar = g.off_raw + ((raw > stg ? raw : stg) + 15) / 16 * 16;
+        g.total = g.off_bar + 2 * NTS * 8 + 16;               // tfull, tempty; min, max, tmem
+        return g;
+    }
+};
+
+namespace tcp {
+// Sorted list of the KL smallest keys: insert lo <= hi (KEY_INF = none).  The k-th smallest of
+// L u {lo, hi} is min(L[k], max(L[k-1], lo), max(L[k-2], hi)).
+template <int KL>
+static __device__ __forceinline__ void ins2(uint32_t (&L)[KL], uint32_t lo, uint32_t hi) {
+#pragma unroll
+    for (int k = KL - 1; k >= 2; --k) L[k] = min(L[k], min(max(L[k - 1], lo), max(L[k - 2], hi)));
+    if (KL >= 2) L[1] = min(L[1], min(max(L[0], lo), hi));
+    L[0] = min(L[0], lo);
+}
+template <int KL>
+static __device__ __forceinline__ void ins1(uint32_t (&L)[KL], uint32_t x) {
+#pragma unroll
+    for (int k = KL - 1; k >= 1; --k) L[k] = min(L[k], max(L[k - 1], x));
+    L[0] = min(L[0], x);
+}
+// step coprime to n near 0.618 n (scrambled row order)
+static __device__ __forceinline__ int row_step(int n) {
+    int st = max(1, (int)(0.618f * (float)n));
+    for (;; ++st) {
+        int x = st, y = n;
+        while (y) {
+            const int t = x % y;
+            x = y;
+            y = t;
+        }
+        if (x == 1) return st;
+    }
+}
+static __device__ __forceinline__ uint32_t win_bits(int lo, int hi, int k) {
+    const int a0 = max(lo, 32 * k), a1 = min(hi, 32 * k + 31);
+    if (a0 > a1) return 0u;
+    const int nb = a1 - a0 + 1;
+    return (nb == 32 ? 0xffffffffu : ((1u << nb) - 1u)) << (a0 - 32 * k);
+}
+}  // namespace tcp
+
+template <int P, int S, int KL>
+__global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams p, int mmax) {
+    using namespace tcp;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const TcpGeom g = TcpGeom::make(P, S, p.r);
+    const int r = p.r, cb = p.cb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kr1 = min(p.row_end, p.Ry_reg);
+    const int gy0 = p.row_begin + TY * (int)blockIdx.y, gx0 = TX * (int)blockIdx.x;
+    const int bimg = blockIdx.z;
+    const int cy0 = gy0 * S - r, cx0 = gx0 * S - r;  // image position of candidate (t, j) = (0, 0)
+    const int ylo = max(0, p.slab_y0), yhi = min(p.H, p.slab_y1);
+    const int16_t* __restrict__ img = p.img + (int64_t)bimg * p.img_bstride;
+    int16_t* const raw = reinterpret_cast<int16_t*>(sm + g.off_raw);
+    float* const nq = reinterpret_cast<float*>(sm + g.off_nq);
+    int* const hs = reinterpret_cast<int*>(sm + g.off_x);
+    uint64_t* const tfull = reinterpret_cast<uint64_t*>(sm + g.off_bar);
+    uint64_t* const tempty = tfull + NTS;
+    int* const misc = reinterpret_cast<int*>(tempty + NTS);  // zmin, zmax, TMEM address
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NTS; ++i) {
+            tc::mbar_init(&tfull[i], 1);
+            tc::mbar_init(&tempty[i], EPI_WARPS);
+        }
+        misc[0] = INT_MAX;
+        misc[1] = INT_MIN;
+        tc::fence_mbar_init();
+    }
+    if (warp == MMA_WARP) tc::tmem_alloc<TMEM_COLS>(reinterpret_cast<uint32_t*>(misc + 2));
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = static_cast<uint32_t>(misc[2]);
+
+    // (1) int16 pixel plane of the tile (0 outside the image / slab and beyond the used columns)
+    // and the range of the used pixels
+    const int ucols = g.NJ + P - 1;
+    {
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int i = threadIdx.x; i < g.PR * PW; i += THREADS) {
+            const int y = i / PW, x = i - y * PW;
+            const int gy = cy0 + y, gx = cx0 + x;
+            int v = 0;
+            if (x < ucols && gy >= ylo && gy < yhi && gx >= 0 && gx < p.W) {
+                v = img[(int64_t)(gy - p.slab_y0) * p.W + gx];
+                lo = min(lo, v);
+                hi = max(hi, v);
+            }
+            raw[i] = (int16_t)v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            atomicMin(&misc[0], lo);
+            atomicMax(&misc[1], hi);
+        }
+    }
+    __syncthreads();
+    const int zmin = misc[0], zmax = misc[1];
+    const int cz = (zmin + zmax) >> 1;
+    const bool fast = max(zmax - cz, cz - zmin) <= mmax;
+
+    // the tile's candidate rows: in the image (slab) and in some valid reference's window
+    const int amax = min(TY, kr1 - gy0) - 1;
+    const int t_lo = max(0, ylo - cy0);
+    const int t_hi = min(min(g.NT - 1, (yhi - P) - cy0), amax * S + 2 * r);
+    const int nrow = t_hi - t_lo + 1;
+
+    if (fast) {
+        // (2) horizontal sums of squares of z - c (int32) in the X region
+        for (int i = threadIdx.x; i < g.PR * NB; i += THREADS) {
+            const int y = i / NB, j = i - y * NB;
+            const int16_t* rw = raw + y * PW + j;
+            int s = 0;
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+                const int d = (int)rw[jj] - cz;
+                s += d * d;
+            }
+            hs[i] = s;
+        }
+        __syncthreads();
+        // (3) candidate norms N_q (P x P box sums; integers <= 2^24, exact in fp32); +inf for
+        // candidates outside the image or the tile's columns (they never pass)
+        for (int i = threadIdx.x; i < g.NT * NB; i += THREADS) {
+            const int t = i / NB, j = i - t * NB;
+            const int cy = cy0 + t, cx = cx0 + j;
+            float v = __int_as_float(0x7f800000);
+            if (j < g.NJ && cy >= ylo && cy <= yhi - P && cx >= 0 && cx <= p.W - P) {
+                int s = 0;
+#pragma unroll
+                for (int ii = 0; ii < P; ++ii) s += hs[(t + ii) * NB + j];
+                v = (float)s;
+            }
+            nq[i] = v;
+        }
+        __syncthreads();
+        // (4) X: pre-shifted centred fp16 rows (pixels outside the used area are finite and only
+        // feed masked candidates or the zero columns of A)
+        for (int i = threadIdx.x; i < (g.PR + 1) * XQ * 8; i += THREADS) {
+            const int y = i / (XQ * 8), rem = i - y * (XQ * 8);
+            const int q = rem >> 3, m = rem & 7;
+            const int x0 = 8 * q + m;
+            uint32_t hw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int v0 = (y < g.PR ? (int)raw[y * PW + x0 + 2 * e] : 0) - cz;
+                const int v1 = (y < g.PR ? (int)raw[y * PW + x0 + 2 * e + 1] : 0) - cz;
+                const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
+                hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(sm + g.off_x + y * XP + q * 128 + m * 16) =
+                make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        }
+        // (5) A: TMEM lane m = reference m holds its patch, K = 16 i + j (j >= P zero), two fp16
+        // per column; epilogue warp w writes its lane quarter
+        if (warp < EPI_WARPS) {
+            const int m = 32 * warp + lane, a = m >> 3, b = m & 7;
+            const int16_t* rp = raw + (a * S + r) * PW + b * S + r;
+#pragma unroll
+            for (int c3 = 0; c3 < (P * 8 + 31) / 32; ++c3) {
+                uint32_t av[32];
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int i = 4 * c3 + ii;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int j0 = 2 * e, j1 = 2 * e + 1;
+                        const int v0 = (i < P && j0 < P) ? (int)rp[i * PW + j0] - cz : 0;
+                        const int v1 = (i < P && j1 < P) ? (int)rp[i * PW + j1] - cz : 0;
+                        const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
+                        av[8 * ii + e] = *reinterpret_cast<const uint32_t*>(&h2);
+                    }
+                }
+                tc::tmem_st32(tmem + TM_A + 32 * c3 + ((uint32_t)(32 * warp) << 16), av);
+            }
+            tc::tmem_wait_st();
+        }
+        tc::fence_proxy_async_smem();  // generic-proxy X stores -> the tensor core
+        tc::tc_fence_before();
+    }
+    __syncthreads();
+    tc::tc_fence_after();
+
+    if (warp == MMA_WARP) {
+        // ---------------- MMA issuer: 12 x (M128 N80 K16) per candidate row; lane 0 issues
+        if (fast && nrow > 0) {
+            const uint32_t idesc = tc::idesc_f16f16_f32(128, NB);
+            const uint32_t xa = tc::smem_u32(sm + g.off_x);
+            const int step = row_step(nrow);
+            int tc_ = 0;
+            for (int s = 0; s < nrow; ++s) {
+                const int ts = s % NTS, t = t_lo + tc_;
+                tc_ += step;
+                if (tc_ >= nrow) tc_ -= nrow;
+                if (s >= NTS) tc::mbar_wait(&tempty[ts], ((s / NTS) - 1) & 1);
+                tc::tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < P; ++i)
+                        tc::mma_f16_ts(tmem + (uint32_t)(ts * SPITCH), tmem + TM_A + 8 * i,
+                                       tc::smem_desc(xa + (uint32_t)((t + i) * XP), 128, 128), idesc,
+                                       i > 0 ? 1u : 0u);
+                    tc::mma_commit(&tfull[ts]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < EPI_WARPS) {
+        // ---------------- warp w: references of TMEM lane quarter w (lane = reference)
+        const int m = 32 * warp + lane, a = m >> 3, b = m & 7;
+        const int ky = gy0 + a, kx = gx0 + b;
+        const bool active = ky < kr1 && kx < p.Rx_reg;
+        const int ry = ky * S, rx = kx * S;  // regular grid positions
+        const int nfill = KL - (p.K - 1);    // sentinel zeros below the real keys
+        uint32_t L[KL];
+#pragma unroll
+        for (int i = 0; i < KL; ++i) L[i] = i < nfill ? 0u : KEY_INF;
+        const int tdr0 = p.tdr0;
+        if (fast) {
+            const float Np = nq[(a * S + r) * NB + b * S + r];
+            const int wlo = b * S, whi = b * S + 2 * r;
+            const uint32_t w0 = active ? win_bits(wlo, whi, 0) : 0u;
+            const uint32_t w1 = active ? win_bits(wlo, whi, 1) : 0u;
+            const uint32_t w2 = active ? win_bits(wlo, whi, 2) : 0u;
+            float* const stg = reinterpret_cast<float*>(sm + g.off_raw) + (32 * warp + lane) * STG_PITCH;
+            const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
+            const int trow0 = 4 * warp * S, trow1 = (4 * warp + 3) * S + 2 * r;
+            float T = (float)(tdr0 + 1) - Np;
+            const int step = nrow > 0 ? row_step(nrow) : 1;
+            int tc_ = 0;
+            for (int s = 0; s < nrow; ++s) {
+                const int ts = s % NTS, t = t_lo + tc_;
+                tc_ += step;
+                if (tc_ >= nrow) tc_ -= nrow;
+                tc::mbar_wait(&tfull[ts], (s / NTS) & 1);
+                tc::tc_fence_after();
+                if (t < trow0 || t > trow1) {  // no reference of this warp uses row t
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                    continue;
+                }
+                uint32_t acc[NB];
+#pragma unroll
+                for (int c = 0; c < NB / 16; ++c)
+                    tc::tmem_ld16p(taddr + (uint32_t)(ts * SPITCH + 16 * c), acc + 16 * c);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < NB / 16; ++c) tc::tmem_tie16(acc + 16 * c);
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&tempty[ts]);
+                // u = N_q - 2 <f_p, f_q> (exact for every passing candidate), staged; pass bits
+                // = sign of u - T, bit j of word j / 32
+                const float* nqr = nq + t * NB;
+                uint32_t mk[3] = {0u, 0u, 0u};
+#pragma unroll
+                for (int c = NB / 4 - 1; c >= 0; --c) {
+                    const float4 n4 = *reinterpret_cast<const float4*>(nqr + 4 * c);
+                    const float nv[4] = {n4.x, n4.y, n4.z, n4.w};
+                    float u[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = fmaf(-2.f, __uint_as_float(acc[4 * c + e]), nv[e]);
+                    *reinterpret_cast<float4*>(stg + 4 * c) = make_float4(u[0], u[1], u[2], u[3]);
+#pragma unroll
+                    for (int e = 3; e >= 0; --e) {
+                        const int j = 4 * c + e;
+                        mk[j >> 5] = __funnelshift_l(__float_as_uint(u[e] - T), mk[j >> 5], 1);
+                    }
+                }
+                const int tt = t - a * S;
+                const bool rowok = (unsigned)tt <= (unsigned)(2 * r);
+                uint32_t m0 = rowok ? (mk[0] & w0) : 0u, m1 = rowok ? (mk[1] & w1) : 0u,
+                         m2 = rowok ? (mk[2] & w2) : 0u;
+                if (tt == r) {  // the reference itself (slot 0)
+                    const int js = b * S + r;
+                    if (js < 32) m0 &= ~(1u << js);
+                    else if (js < 64) m1 &= ~(1u << (js - 32));
+                    else m2 &= ~(1u << (js - 64));
+                }
+                const uint32_t cbase = (uint32_t)(tt * p.side - b * S);
+                auto pop = [&]() -> uint32_t {
+                    int j;
+                    if (m0) {
+                        j = __ffs(m0) - 1;
+                        m0 &= m0 - 1u;
+                    } else if (m1) {
+                        j = 31 + __ffs(m1);
+                        m1 &= m1 - 1u;
+                    } else if (m2) {
+                        j = 63 + __ffs(m2);
+                        m2 &= m2 - 1u;
+                    } else {
+                        return KEY_INF;
+                    }
+                    return (__float2uint_rn(stg[j] + Np) << cb) | (cbase + (uint32_t)j);
+                };
+                while (__any_sync(0xffffffffu, (m0 | m1 | m2) != 0u)) {
+                    const uint32_t k1 = pop(), k2 = pop();
+                    ins2<KL>(L, min(k1, k2), max(k1, k2));
+                }
+                const int gd = min((int)(L[KL - 1] >> cb), tdr0);
+                T = (float)(gd + 1) - Np;
+            }
+        } else if (active) {
+            // ---------------- exact int32 path for a tile above the fp16 bound: direct Eq. (1)
+            const int pa = a * S + r, pb = b * S + r;  // the reference's plane position
+            for (int dy = -r; dy <= r; ++dy) {
+                const int cy = ry + dy;
+                if (cy < ylo || cy > yhi - P) continue;
+                for (int dx = -r; dx <= r; ++dx) {
+                    const int cx = rx + dx;
+                    if (cx < 0 || cx > p.W - P || (dy == 0 && dx == 0)) continue;
+                    int d = 0;
+                    for (int i = 0; i < P; ++i) {
+                        const int16_t* r0 = raw + (pa + i) * PW + pb;
+                        const int16_t* r1 = raw + (pa + dy + i) * PW + pb + dx;
+#pragma unroll
+                        for (int jj = 0; jj < P; ++jj) {
+                            const int df = (int)r0[jj] - (int)r1[jj];
+                            d += df * df;
+                        }
+                    }
+                    if (d <= tdr0)
+                        ins1<KL>(L, ((uint32_t)d << cb) | (uint32_t)((dy + r) * p.side + dx + r));
+                }
+            }
+        }
+        // ---------------- output: slot 0 = self, ranks 1 .. K-1, pads (self, -1)
+        if (active) {
+            const int self = ry * p.W + rx;
+            const int64_t ref = (int64_t)bimg * p.out_bstride + (int64_t)(ky - p.row_begin) * p.Rx + kx;
+            int32_t* const oi = p.idx + ref * p.K;
+            int32_t* const od = p.dist + ref * p.K;
+            oi[0] = self;
+            od[0] = 0;
+            int cnt = 0;
+            const uint32_t cmask = (1u << cb) - 1u;
+#pragma unroll
+            for (int i = 0; i < KL; ++i) {
+                const int s = i - nfill + 1;
+                if (s >= 1) {
+                    const uint32_t key = L[i];
+                    if (key != KEY_INF) {
+                        const int code = (int)(key & cmask);
+                        const int dy = code / p.side - r, dx = code - (code / p.side) * p.side - r;
+                        oi[s] = (ry + dy) * p.W + rx + dx;
+                        od[s] = (int)(key >> cb);
+                        ++cnt;
+                    } else {
+                        oi[s] = self;
+                        od[s] = -1;
+                    }
+                }
+            }
+            if (p.nvalid) p.nvalid[ref] = 1 + cnt;
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == MMA_WARP) tc::tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// Largest tile half-range M with P^2 M^2 <= 2^24 (and |z - c| <= 2048 for fp16).
+static inline int tcp_default_mmax(int P) {
+    int M = 0;
+    while (M < 2048 && (long long)P * P * (M + 1) * (M + 1) <= (1LL << 24)) ++M;
+    return M;
+}
+
+template <int P, int S, int KL>
+cudaError_t launch_tcp(const MatchParams& p, cudaStream_t stream, int* launches) {
+    const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
+    if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
+    const TcpGeom g = TcpGeom::make(P, S, p.r);
+    auto kern = match_tcp_kernel<P, S, KL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.total);
+    if (e != cudaSuccess) return e;
+    // dev / test switch: a lower bound forces tiles onto the exact int32 path
+    static const int mmax_env = getenv("GBM3D_TCP_MMAX") ? atoi(getenv("GBM3D_TCP_MMAX")) : -1;
+    const int mmax = mmax_env >= 0 ? mmax_env : tcp_default_mmax(P);
+    dim3 grid((p.Rx_reg + tcp::TX - 1) / tcp::TX, (kr1 - kr0 + tcp::TY - 1) / tcp::TY, p.B);
+    kern<<<grid, tcp::THREADS, g.total, stream>>>(p, mmax);
+    if (launches) ++*launches;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    static const bool dbg = getenv("GBM3D_DEBUG") != nullptr;
+    if (dbg) {
+        e = cudaStreamSynchronize(stream);
+        fprintf(stderr, "gbm3d: tcp P%d S%d grid %u x %u x %u smem %d: %s\n", P, S, grid.x, grid.y,
+                grid.z, g.total, cudaGetErrorString(e));
+    }
+    return e;
+}
+
+}  // namespace gbm3d

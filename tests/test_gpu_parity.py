@@ -46,9 +46,15 @@ def _oracle_config(name, ci):
     return oracle.block_match(imgs[0], c.patch, c.stride, c.radius, c.K, c.tau)
 
 
-def _product_supported(P, s, r, K):
-    """Shapes the tensor-core product kernels take (include/gbm3d.h, GBM3D_METHOD_PRODUCT)."""
-    return P == 8 and s == 3 and 7 * s + 2 * r + 1 <= 64 and 2 <= K <= 32
+def _product_supported(P, s, r, K, tau=None, method="product"):
+    """Shapes the tensor-core product kernels take (include/gbm3d.h, GBM3D_METHOD_PRODUCT):
+    P8 s3 r<=21 (fp16 and int8 kernels); P12 s4 r<=21 with tau - 1 within the 32-bit key's
+    d range (fp16 kernel only)."""
+    if P == 8 and s == 3:
+        return 7 * s + 2 * r + 1 <= 64 and 2 <= K <= 32
+    if P == 12 and s == 4 and method == "product":
+        return r <= 21 and 2 <= K <= 32 and tau is not None and tau - 1 <= (1 << 21) - 1
+    return False
 
 
 # ----------------------------------------------------------------- the five BASELINE configs
@@ -128,9 +134,9 @@ def test_edge_cases(H, W, P, s, r, K, tau, kind):
                  f"{kind} {H}x{W} P{P} s{s} r{r} K{K} tau{tau}")
 
 
-@pytest.mark.parametrize("method", ["product", "product_i8"])
-@pytest.mark.parametrize("H,W,P,s,r,K,tau,kind",
-                         [e for e in EDGE if _product_supported(e[2], e[3], e[4], e[5])])
+@pytest.mark.parametrize("method,H,W,P,s,r,K,tau,kind",
+                         [(m,) + e for m in ("product", "product_i8") for e in EDGE
+                          if _product_supported(e[2], e[3], e[4], e[5], e[6], m)])
 def test_edge_cases_product(H, W, P, s, r, K, tau, kind, method):
     img = special_image(kind, H, W, seed=H * 1000 + W, lo=-250, hi=500, value=77)
     _assert_same(_gpu(img, P, s, r, K, tau, method=method), oracle.block_match(img, P, s, r, K, tau),
@@ -151,8 +157,95 @@ def test_product_mixed_range_tiles():
 def test_product_unsupported_shape_reports():
     g = _gbm3d()
     img = torch.from_numpy(config_images("c2")[0]).cuda()
-    with pytest.raises(g.GBM3DError):
-        g.block_match(img, 12, 4, 19, 16, 720000, method="product")
+    with pytest.raises(g.GBM3DError):   # P12 without tau: keys beyond the 32-bit d range
+        g.block_match(img, 12, 4, 19, 16, None, method="product")
+    with pytest.raises(g.GBM3DError):   # no int8 kernel for P12
+        g.block_match(img, 12, 4, 19, 16, 720000, method="product_i8")
+    with pytest.raises(g.GBM3DError):   # radius above the P12 shared-memory bound
+        g.block_match(img, 12, 4, 22, 16, 720000, method="product")
+
+
+P12_CASES = [
+    # H, W, r, K, tau, kind: ragged tiles, windows clipped at every border, K and tau extremes
+    (61, 59, 19, 16, 720000, "uniform"),
+    (130, 75, 19, 32, 720000, "uniform"),
+    (100, 140, 21, 16, 500000, "uniform"),
+    (90, 90, 5, 2, 1000000, "uniform"),
+    (70, 66, 0, 16, 100, "uniform"),        # r = 0: only the reference
+    (80, 80, 19, 16, 0, "uniform"),         # tau = 0: nothing passes
+    (76, 92, 19, 16, 2097152, "uniform"),   # tau - 1 = dsat exactly
+    (70, 90, 19, 16, 720000, "constant"),   # all-zero distances: pure tie order
+    (70, 90, 19, 32, 720000, "periodic"),
+    (70, 90, 19, 16, 720000, "checker"),
+    (12, 12, 19, 16, 5000, "uniform"),      # one reference
+]
+
+
+@pytest.mark.parametrize("H,W,r,K,tau,kind", P12_CASES)
+def test_p12_product_edge_cases(H, W, r, K, tau, kind):
+    """The patch-12 tensor-core kernel (AUTO for c2's shape) on ragged, clipped and degenerate
+    inputs, bit-exact against the oracle."""
+    img = special_image(kind, H, W, seed=H * 1000 + W, lo=-150, hi=400, value=77)
+    exp = oracle.block_match(img, 12, 4, r, K, tau)
+    _assert_same(_gpu(img, 12, 4, r, K, tau, method="product"), exp, f"P12 {kind} {H}x{W} r{r} K{K}")
+    _assert_same(_gpu(img, 12, 4, r, K, tau), exp, f"P12 auto {kind} {H}x{W} r{r} K{K}")
+
+
+@pytest.mark.parametrize("H,W,r,K,tau,sigma,seed", [
+    (140, 130, 19, 16, 720000, 50.0, 1),
+    (97, 151, 19, 32, 400000, 25.0, 2),
+    (120, 100, 21, 16, 2000000, 10.0, 3),
+    (64, 200, 13, 8, 90000, 5.0, 4),
+])
+def test_p12_product_natural(H, W, r, K, tau, sigma, seed):
+    """Natural-looking images (filled lists, ties between flat-region candidates) through the
+    patch-12 tensor-core kernel, bit-exact against the oracle, single and batched."""
+    from synth import make_image
+    img = make_image(H, W, 12, 3, sigma, seed)
+    exp = oracle.block_match(img, 12, 4, r, K, tau)
+    _assert_same(_gpu(img, 12, 4, r, K, tau, method="product"), exp, f"P12 natural {H}x{W}")
+    imgs = np.stack([img, make_image(H, W, 6, 2, sigma, seed + 50)])
+    g = _gbm3d()
+    i, d, n = g.block_match(torch.from_numpy(imgs).cuda(), 12, 4, r, K, tau, method="product")
+    eb = oracle.block_match_batched(imgs, 12, 4, r, K, tau)
+    _assert_same((i.cpu().numpy(), d.cpu().numpy(), n.cpu().numpy()), eb, "P12 natural batched")
+
+
+def test_p12_product_exact_int_path(monkeypatch):
+    """Tiles above the fp16 exactness bound take the kernel's exact int32 path: with the bound
+    forced to 0 (dev switch GBM3D_TCP_MMAX, read once per process -> a subprocess) every tile
+    does, and the c2 table plus a mixed-range image still match the oracle."""
+    import subprocess, sys, os, json
+    code = r'''
+import numpy as np, torch, json, sys
+import paper_2103_10765_b200 as g
+from synth import config_images
+img = config_images("c2")[0][:200, :180].copy()
+rng = np.random.default_rng(3)
+img2 = rng.integers(-100, 356, size=(150, 170)).astype(np.int16)
+img2[60:110, 20:90] = rng.choice(np.array([-900, 900], np.int16), size=(50, 70))
+out = []
+for im, tau in ((img, 720000), (img2, 2000000)):
+    i, d, n = g.block_match(torch.from_numpy(im).cuda(), 12, 4, 19, 16, tau, method="product")
+    out.append([i.cpu().numpy().tolist(), d.cpu().numpy().tolist(), n.cpu().numpy().tolist()])
+json.dump(out, sys.stdout)
+'''
+    rng = np.random.default_rng(3)
+    img2 = rng.integers(-100, 356, size=(150, 170)).astype(np.int16)
+    img2[60:110, 20:90] = rng.choice(np.array([-900, 900], np.int16), size=(50, 70))
+    cases = ((config_images("c2")[0][:200, :180].copy(), 720000), (img2, 2000000))
+    for mmax in ("0", None):
+        env = dict(os.environ)
+        if mmax is not None:
+            env["GBM3D_TCP_MMAX"] = mmax
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = json.loads(r.stdout)
+        for (im, tau), gg in zip(cases, got):
+            exp = oracle.block_match(im, 12, 4, 19, 16, tau)
+            _assert_same(tuple(np.array(x, dtype=np.int32) for x in gg), exp,
+                         f"P12 exact path mmax={mmax} tau={tau}")
 
 
 @pytest.mark.parametrize("seed", range(12))
