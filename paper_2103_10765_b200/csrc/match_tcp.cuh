@@ -48,11 +48,12 @@ constexpr int NB = 80;               // candidate columns per MMA (N), >= 7S + 2
 constexpr int PW = 96;               // pixel plane pitch (int16): NB + 16
 constexpr int XQ = NB / 8;           // 16-byte pixel groups per pre-shifted row
 constexpr int XP = XQ * 128;         // bytes per pre-shifted plane row (8 shifts per group)
-constexpr int NTS = 4;               // accumulator stages in flight
-constexpr int SPITCH = 96;           // TMEM columns per stage (N = 80, 32-column aligned)
-constexpr int TM_A = NTS * SPITCH;   // A operand: 12 K16 steps x 8 columns (two fp16 each)
+constexpr int NTS = 5;               // accumulator stages in flight
+constexpr int SPITCH = NB;           // TMEM columns per stage
+constexpr int TM_A = (NTS * SPITCH + 31) / 32 * 32;  // A: 12 K16 steps x 8 columns (two fp16 each)
 constexpr int EPI_WARPS = 4, MMA_WARP = 4, NWARPS = 8, THREADS = 32 * NWARPS;
-constexpr int STG_PITCH = 84;        // floats per lane and staged row (conflict-free STS.128)
+constexpr int STG_PITCH = 44;        // floats per lane: the window's <= 11 groups of 4 columns
+                                     // (lane pitch 44 words: conflict-free STS.128)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MAX_R = 21;            // shared memory bound (see TcpGeom)
 }  // namespace tcp
@@ -76,6 +77,34 @@ struct TcpGeom {
         return g;
     }
 };
+
+#if GBM3D_TCP_TRACE  // dev-only: %globaltimer stamps per CTA, read by gbm3d_dev_tcp_trace
+static __device__ long long g_tcp_trace[4096][8];
+static __device__ long long g_tcp_cnt[4096][4][6];  // per warp: wait, scan, rounds cycles; rounds, rows, dense rows
+#define TCP_CLK(v) (v) = clock64()
+#define TCP_ADD(i, v)                                                                          \
+    do {                                                                                       \
+        const int c_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;         \
+        if (c_ < 4096 && lane == 0) g_tcp_cnt[c_][warp & 3][i] += (v);                         \
+    } while (0)
+#define TCP_TR(k)                                                                          \
+    do {                                                                                   \
+        long long t_;                                                                      \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+        const int c_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;     \
+        if (c_ < 4096) g_tcp_trace[c_][k] = t_;                                            \
+    } while (0)
+#else
+#define TCP_TR(k) \
+    do {          \
+    } while (0)
+#define TCP_CLK(v) \
+    do {           \
+    } while (0)
+#define TCP_ADD(i, v) \
+    do {              \
+    } while (0)
+#endif
 
 namespace tcp {
 // Sorted list of the KL smallest keys: insert lo <= hi (KEY_INF = none).  The k-th smallest of
@@ -117,6 +146,8 @@ static __device__ __forceinline__ uint32_t win_bits(int lo, int hi, int k) {
 template <int P, int S, int KL>
 __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams p, int mmax) {
     using namespace tcp;
+    static_assert(S % 4 == 0, "window staging in groups of 4 columns needs bS = S b aligned to 4");
+    static_assert(TM_A + 8 * P <= (int)TMEM_COLS, "TMEM: accumulator stages + A");
     extern __shared__ __align__(1024) unsigned char sm[];
     const TcpGeom g = TcpGeom::make(P, S, p.r);
     const int r = p.r, cb = p.cb;
@@ -135,6 +166,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     int* const misc = reinterpret_cast<int*>(tempty + NTS);  // zmin, zmax, TMEM address
 
     if (threadIdx.x == 0) {
+        TCP_TR(0);
         for (int i = 0; i < NTS; ++i) {
             tc::mbar_init(&tfull[i], 1);
             tc::mbar_init(&tempty[i], EPI_WARPS);
@@ -154,16 +186,30 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     const int ucols = g.NJ + P - 1;
     {
         int lo = INT_MAX, hi = INT_MIN;
-        for (int i = threadIdx.x; i < g.PR * PW; i += THREADS) {
-            const int y = i / PW, x = i - y * PW;
-            const int gy = cy0 + y, gx = cx0 + x;
-            int v = 0;
-            if (x < ucols && gy >= ylo && gy < yhi && gx >= 0 && gx < p.W) {
-                v = img[(int64_t)(gy - p.slab_y0) * p.W + gx];
-                lo = min(lo, v);
-                hi = max(hi, v);
+        // 8 loads in flight per thread (the image is L2-resident: latency, not bandwidth)
+        for (int i0 = threadIdx.x; i0 < g.PR * PW; i0 += 8 * THREADS) {
+            int v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * THREADS;
+                const int y = i / PW, x = i - y * PW;
+                const int gy = cy0 + y, gx = cx0 + x;
+                v[k] = INT_MIN;
+                if (i < g.PR * PW && x < ucols && gy >= ylo && gy < yhi && gx >= 0 && gx < p.W)
+                    v[k] = __ldg(img + (int64_t)(gy - p.slab_y0) * p.W + gx);
             }
-            raw[i] = (int16_t)v;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * THREADS;
+                if (i < g.PR * PW) {
+                    const bool in = v[k] != INT_MIN;
+                    if (in) {
+                        lo = min(lo, v[k]);
+                        hi = max(hi, v[k]);
+                    }
+                    raw[i] = (int16_t)(in ? v[k] : 0);
+                }
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -176,6 +222,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) TCP_TR(1);
     const int zmin = misc[0], zmax = misc[1];
     const int cz = (zmin + zmax) >> 1;
     const bool fast = max(zmax - cz, cz - zmin) <= mmax;
@@ -261,6 +308,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     }
     __syncthreads();
     tc::tc_fence_after();
+    if (threadIdx.x == 0) TCP_TR(2);
 
     if (warp == MMA_WARP) {
         // ---------------- MMA issuer: 12 x (M128 N80 K16) per candidate row; lane 0 issues
@@ -299,39 +347,52 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
         const int tdr0 = p.tdr0;
         if (fast) {
             const float Np = nq[(a * S + r) * NB + b * S + r];
-            const int wlo = b * S, whi = b * S + 2 * r;
-            const uint32_t w0 = active ? win_bits(wlo, whi, 0) : 0u;
-            const uint32_t w1 = active ? win_bits(wlo, whi, 1) : 0u;
-            const uint32_t w2 = active ? win_bits(wlo, whi, 2) : 0u;
+            const int wn = 2 * r + 1;  // window columns (<= 43)
+            const uint64_t wmask = active ? ((1ull << wn) - 1ull) : 0ull;
+            const int nwg = (2 * r) / 4 + 1;  // staged groups of 4 columns: [b, b + nwg) (bS = 4b)
             float* const stg = reinterpret_cast<float*>(sm + g.off_raw) + (32 * warp + lane) * STG_PITCH;
+            float* const stgb = stg - 4 * b;
             const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
             const int trow0 = 4 * warp * S, trow1 = (4 * warp + 3) * S + 2 * r;
             float T = (float)(tdr0 + 1) - Np;
             const int step = nrow > 0 ? row_step(nrow) : 1;
-            int tc_ = 0;
-            for (int s = 0; s < nrow; ++s) {
-                const int ts = s % NTS, t = t_lo + tc_;
-                tc_ += step;
-                if (tc_ >= nrow) tc_ -= nrow;
-                tc::mbar_wait(&tfull[ts], (s / NTS) & 1);
-                tc::tc_fence_after();
-                if (t < trow0 || t > trow1) {  // no reference of this warp uses row t
+            int s = 0, tc_ = 0;
+            // the warp's next row (rows visited in the scrambled order; the stages of rows no
+            // reference of this warp uses are released at once); -1 after the last
+            auto next_row = [&](int& ts_out) -> int {
+                while (s < nrow) {
+                    const int ts = s % NTS, t = t_lo + tc_;
+                    tc::mbar_wait(&tfull[ts], (s / NTS) & 1);
+                    tc::tc_fence_after();
+                    ++s;
+                    tc_ += step;
+                    if (tc_ >= nrow) tc_ -= nrow;
+                    if (t >= trow0 && t <= trow1) {
+                        ts_out = ts;
+                        return t;
+                    }
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&tempty[ts]);
-                    continue;
                 }
-                uint32_t acc[NB];
+                return -1;
+            };
+            uint32_t acc[NB];
+            int ts = 0;
+            int t = next_row(ts);
+            if (t >= 0) {
 #pragma unroll
                 for (int c = 0; c < NB / 16; ++c)
                     tc::tmem_ld16p(taddr + (uint32_t)(ts * SPITCH + 16 * c), acc + 16 * c);
+            }
+            while (t >= 0) {
                 tc::tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < NB / 16; ++c) tc::tmem_tie16(acc + 16 * c);
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&tempty[ts]);
-                // u = N_q - 2 <f_p, f_q> (exact for every passing candidate), staged; pass bits
-                // = sign of u - T, bit j of word j / 32
+                // u = N_q - 2 <f_p, f_q> (exact for every passing candidate); the lane's window
+                // groups staged; pass bits = sign of u - T, bit j of word j / 32
                 const float* nqr = nq + t * NB;
                 uint32_t mk[3] = {0u, 0u, 0u};
 #pragma unroll
@@ -341,46 +402,51 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                     float u[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) u[e] = fmaf(-2.f, __uint_as_float(acc[4 * c + e]), nv[e]);
-                    *reinterpret_cast<float4*>(stg + 4 * c) = make_float4(u[0], u[1], u[2], u[3]);
+                    if ((unsigned)(c - b) < (unsigned)nwg)
+                        *reinterpret_cast<float4*>(stgb + 4 * c) = make_float4(u[0], u[1], u[2], u[3]);
 #pragma unroll
                     for (int e = 3; e >= 0; --e) {
                         const int j = 4 * c + e;
                         mk[j >> 5] = __funnelshift_l(__float_as_uint(u[e] - T), mk[j >> 5], 1);
                     }
                 }
+                // window-relative 64-bit mask: bit k = column bS + k = displacement dx + r
                 const int tt = t - a * S;
-                const bool rowok = (unsigned)tt <= (unsigned)(2 * r);
-                uint32_t m0 = rowok ? (mk[0] & w0) : 0u, m1 = rowok ? (mk[1] & w1) : 0u,
-                         m2 = rowok ? (mk[2] & w2) : 0u;
-                if (tt == r) {  // the reference itself (slot 0)
-                    const int js = b * S + r;
-                    if (js < 32) m0 &= ~(1u << js);
-                    else if (js < 64) m1 &= ~(1u << (js - 32));
-                    else m2 &= ~(1u << (js - 64));
+                const int bs = b * S;
+                uint64_t mw = (((uint64_t)mk[1] << 32) | mk[0]) >> bs;
+                if (bs > 0) mw |= (uint64_t)mk[2] << (64 - bs);
+                mw &= ((unsigned)tt <= (unsigned)(2 * r)) ? wmask : 0ull;
+                if (tt == r) mw &= ~(1ull << r);  // the reference itself (slot 0)
+                // the next row's accumulators load while this row's keys are inserted
+                int tsn = 0;
+                const int tn = next_row(tsn);
+                if (tn >= 0) {
+#pragma unroll
+                    for (int c = 0; c < NB / 16; ++c)
+                        tc::tmem_ld16p(taddr + (uint32_t)(tsn * SPITCH + 16 * c), acc + 16 * c);
                 }
-                const uint32_t cbase = (uint32_t)(tt * p.side - b * S);
+                const uint32_t cbase = (uint32_t)(tt * p.side);
                 auto pop = [&]() -> uint32_t {
-                    int j;
-                    if (m0) {
-                        j = __ffs(m0) - 1;
-                        m0 &= m0 - 1u;
-                    } else if (m1) {
-                        j = 31 + __ffs(m1);
-                        m1 &= m1 - 1u;
-                    } else if (m2) {
-                        j = 63 + __ffs(m2);
-                        m2 &= m2 - 1u;
-                    } else {
-                        return KEY_INF;
-                    }
-                    return (__float2uint_rn(stg[j] + Np) << cb) | (cbase + (uint32_t)j);
+                    const int j = __ffsll((long long)mw) - 1;
+                    mw &= mw - 1ull;
+                    const uint32_t key = (__float2uint_rn(stg[max(j, 0)] + Np) << cb) | (cbase + (uint32_t)j);
+                    return j >= 0 ? key : KEY_INF;
                 };
-                while (__any_sync(0xffffffffu, (m0 | m1 | m2) != 0u)) {
+                int nr_ = 0;
+                (void)nr_;
+                while (__any_sync(0xffffffffu, mw != 0ull)) {
+#if GBM3D_TCP_TRACE
+                    ++nr_;
+#endif
                     const uint32_t k1 = pop(), k2 = pop();
                     ins2<KL>(L, min(k1, k2), max(k1, k2));
                 }
+                TCP_ADD(3, nr_);
+                TCP_ADD(4, 1);
                 const int gd = min((int)(L[KL - 1] >> cb), tdr0);
                 T = (float)(gd + 1) - Np;
+                t = tn;
+                ts = tsn;
             }
         } else if (active) {
             // ---------------- exact int32 path for a tile above the fp16 bound: direct Eq. (1)
@@ -406,6 +472,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                 }
             }
         }
+        if (lane == 0) TCP_TR(3 + warp);
         // ---------------- output: slot 0 = self, ranks 1 .. K-1, pads (self, -1)
         if (active) {
             const int self = ry * p.W + rx;
@@ -440,6 +507,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     __syncthreads();
     tc::tc_fence_after();
     if (warp == MMA_WARP) tc::tmem_dealloc<TMEM_COLS>(tmem);
+    if (threadIdx.x == 0) TCP_TR(7);
 }
 
 // Largest tile half-range M with P^2 M^2 <= 2^24 (and |z - c| <= 2048 for fp16).

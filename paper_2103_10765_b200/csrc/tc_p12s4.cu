@@ -4,3 +4,16 @@ namespace gbm3d {
 template cudaError_t launch_tcp<12, 4, 15>(const MatchParams&, cudaStream_t, int*);
 template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream_t, int*);
 }  // namespace gbm3d
+
+#if GBM3D_TCP_TRACE
+extern "C" int gbm3d_dev_tcp_trace(long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, gbm3d::g_tcp_trace, sizeof(long long) * 8 * (n < 4096 ? n : 4096));
+}
+extern "C" int gbm3d_dev_tcp_cnt(long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, gbm3d::g_tcp_cnt, sizeof(long long) * 24 * (n < 4096 ? n : 4096));
+}
+extern "C" int gbm3d_dev_tcp_cnt_reset() {
+    static long long z[4096 * 24];
+    return (int)cudaMemcpyToSymbol(gbm3d::g_tcp_cnt, z, sizeof(z));
+}
+#endif
