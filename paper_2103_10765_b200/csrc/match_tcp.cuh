@@ -79,7 +79,7 @@ struct TcpGeom {
 };
 
 #if GBM3D_TCP_TRACE  // dev-only: %globaltimer stamps per CTA, read by gbm3d_dev_tcp_trace
-static __device__ long long g_tcp_trace[4096][8];
+static __device__ long long g_tcp_trace[4096][12];
 static __device__ long long g_tcp_cnt[4096][4][6];  // per warp: wait, scan, rounds cycles; rounds, rows, dense rows
 #define TCP_CLK(v) (v) = clock64()
 #define TCP_ADD(i, v)                                                                          \
@@ -234,70 +234,119 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     const int nrow = t_hi - t_lo + 1;
 
     if (fast) {
-        // (2) horizontal sums of squares of z - c (int32) in the X region
-        for (int i = threadIdx.x; i < g.PR * NB; i += THREADS) {
-            const int y = i / NB, j = i - y * NB;
-            const int16_t* rw = raw + y * PW + j;
-            int s = 0;
+        // (2) the centred fp16 plane in place of the int16 one (pixels outside the used area
+        // become -c: finite, they only feed masked candidates or the zero columns of A)
+        __half* const pl = reinterpret_cast<__half*>(raw);
+        for (int i = threadIdx.x; i < g.PR * PW / 8; i += THREADS) {
+            const uint4 v = *reinterpret_cast<const uint4*>(raw + 8 * i);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            uint32_t h[4];
 #pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-                const int d = (int)rw[jj] - cz;
-                s += d * d;
+            for (int e = 0; e < 4; ++e) {
+                const int v0 = (int)(int16_t)(w[e] & 0xffffu) - cz, v1 = (int)(int16_t)(w[e] >> 16) - cz;
+                const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
+                h[e] = *reinterpret_cast<const uint32_t*>(&h2);
             }
-            hs[i] = s;
+            *reinterpret_cast<uint4*>(raw + 8 * i) = make_uint4(h[0], h[1], h[2], h[3]);
         }
         __syncthreads();
-        // (3) candidate norms N_q (P x P box sums; integers <= 2^24, exact in fp32); +inf for
-        // candidates outside the image or the tile's columns (they never pass)
-        for (int i = threadIdx.x; i < g.NT * NB; i += THREADS) {
-            const int t = i / NB, j = i - t * NB;
-            const int cy = cy0 + t, cx = cx0 + j;
-            float v = __int_as_float(0x7f800000);
-            if (j < g.NJ && cy >= ylo && cy <= yhi - P && cx >= 0 && cx <= p.W - P) {
-                int s = 0;
+        // (3) horizontal sums of squares hs[y][j] = sum_{jj < P} plane[y][j + jj]^2 (fp32, exact:
+        // integers < 2^24 for every used column) into the X region, four columns per task by a
+        // running sum
+        float* const hsf = reinterpret_cast<float*>(hs);
+        for (int i = threadIdx.x; i < g.PR * (NB / 4); i += THREADS) {
+            const int y = i / (NB / 4), gq = i - y * (NB / 4);
+            const uint2* rp = reinterpret_cast<const uint2*>(pl + y * PW + 4 * gq);
+            float sq[16];
 #pragma unroll
-                for (int ii = 0; ii < P; ++ii) s += hs[(t + ii) * NB + j];
-                v = (float)s;
+            for (int k = 0; k < 4; ++k) {
+                const uint2 v = rp[k];
+                const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+                const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+                sq[4 * k] = f0.x * f0.x;
+                sq[4 * k + 1] = f0.y * f0.y;
+                sq[4 * k + 2] = f1.x * f1.x;
+                sq[4 * k + 3] = f1.y * f1.y;
             }
-            nq[i] = v;
+            float s0 = 0.f;
+#pragma unroll
+            for (int k = 0; k < P; ++k) s0 += sq[k];
+            float o[4];
+            o[0] = s0;
+#pragma unroll
+            for (int k = 1; k < 4; ++k) {
+                s0 += sq[P - 1 + k] - sq[k - 1];
+                o[k] = s0;
+            }
+            *reinterpret_cast<float4*>(hsf + y * NB + 4 * gq) = make_float4(o[0], o[1], o[2], o[3]);
         }
         __syncthreads();
-        // (4) X: pre-shifted centred fp16 rows (pixels outside the used area are finite and only
-        // feed masked candidates or the zero columns of A)
+        if (threadIdx.x == 0) TCP_TR(8);
+        // (4) candidate norms N_q (vertical running P-row sums per column and row segment;
+        // integers <= 2^24, exact in fp32); +inf for candidates outside the image or the tile's
+        // columns (they never pass)
+        {
+            constexpr int NSEG = 3;
+            const int seg = (g.NT + NSEG - 1) / NSEG;
+            for (int task = threadIdx.x; task < NB * NSEG; task += THREADS) {
+                const int j = task % NB, sg = task / NB;
+                const int t0 = sg * seg, t1 = min(g.NT, t0 + seg);
+                const int cx = cx0 + j;
+                const bool colok = j < g.NJ && cx >= 0 && cx <= p.W - P;
+                float acc = 0.f;
+#pragma unroll
+                for (int ii = 0; ii < P - 1; ++ii) acc += hsf[(t0 + ii) * NB + j];
+                for (int t = t0; t < t1; ++t) {
+                    acc += hsf[(t + P - 1) * NB + j];
+                    const int cy = cy0 + t;
+                    nq[t * NB + j] = (colok && cy >= ylo && cy <= yhi - P) ? acc : __int_as_float(0x7f800000);
+                    acc -= hsf[t * NB + j];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) TCP_TR(9);
+        // (5) X: pre-shifted rows, X[y][q][m] = plane[y][8q + m .. 8q + m + 7]: a lane per
+        // 16-byte output (consecutive lanes write consecutive chunks: conflict-free), five
+        // 4-byte loads and a byte permute for odd shifts
         for (int i = threadIdx.x; i < (g.PR + 1) * XQ * 8; i += THREADS) {
             const int y = i / (XQ * 8), rem = i - y * (XQ * 8);
             const int q = rem >> 3, m = rem & 7;
-            const int x0 = 8 * q + m;
-            uint32_t hw[4];
+            uint32_t o[4] = {0u, 0u, 0u, 0u};
+            if (y < g.PR) {
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(pl + y * PW) + ((8 * q + m) >> 1);
+                const uint32_t sel = (m & 1) ? 0x5432u : 0x3210u;
+                uint32_t w[5];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int v0 = (y < g.PR ? (int)raw[y * PW + x0 + 2 * e] : 0) - cz;
-                const int v1 = (y < g.PR ? (int)raw[y * PW + x0 + 2 * e + 1] : 0) - cz;
-                const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
-                hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                for (int k = 0; k < 5; ++k) w[k] = wp[k];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] = __byte_perm(w[k], w[k + 1], sel);
             }
-            *reinterpret_cast<uint4*>(sm + g.off_x + y * XP + q * 128 + m * 16) =
-                make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(sm + g.off_x + y * XP + q * 128 + m * 16) = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        // (5) A: TMEM lane m = reference m holds its patch, K = 16 i + j (j >= P zero), two fp16
-        // per column; epilogue warp w writes its lane quarter
+        __syncthreads();
+        // (6) A: TMEM lane m = reference m holds its patch, K = 16 i + j (j >= P zero), two fp16
+        // per column, read from X (patch row i = the 8 pixels at the reference column and the
+        // next P - 8); epilogue warp w writes its lane quarter
         if (warp < EPI_WARPS) {
+            static_assert(P > 8 && P <= 16 && P % 2 == 0, "A rows: one full and one partial 8-pixel chunk");
             const int m = 32 * warp + lane, a = m >> 3, b = m & 7;
-            const int16_t* rp = raw + (a * S + r) * PW + b * S + r;
+            const int col = b * S + r;
+            const unsigned char* xa0 = sm + g.off_x + (a * S + r) * XP + (col >> 3) * 128 + (col & 7) * 16;
 #pragma unroll
             for (int c3 = 0; c3 < (P * 8 + 31) / 32; ++c3) {
                 uint32_t av[32];
 #pragma unroll
                 for (int ii = 0; ii < 4; ++ii) {
                     const int i = 4 * c3 + ii;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int j0 = 2 * e, j1 = 2 * e + 1;
-                        const int v0 = (i < P && j0 < P) ? (int)rp[i * PW + j0] - cz : 0;
-                        const int v1 = (i < P && j1 < P) ? (int)rp[i * PW + j1] - cz : 0;
-                        const __half2 h2 = __halves2half2(__int2half_rn(v0), __int2half_rn(v1));
-                        av[8 * ii + e] = *reinterpret_cast<const uint32_t*>(&h2);
+                    uint4 c0 = make_uint4(0u, 0u, 0u, 0u), c1 = c0;
+                    if (i < P) {
+                        c0 = *reinterpret_cast<const uint4*>(xa0 + i * XP);
+                        c1 = *reinterpret_cast<const uint4*>(xa0 + i * XP + 128);
                     }
+                    const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) av[8 * ii + e] = (2 * e < P) ? cw[e] : 0u;
                 }
                 tc::tmem_st32(tmem + TM_A + 32 * c3 + ((uint32_t)(32 * warp) << 16), av);
             }

@@ -7,7 +7,7 @@ template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream_t, int
 
 #if GBM3D_TCP_TRACE
 extern "C" int gbm3d_dev_tcp_trace(long long* host, int n) {
-    return (int)cudaMemcpyFromSymbol(host, gbm3d::g_tcp_trace, sizeof(long long) * 8 * (n < 4096 ? n : 4096));
+    return (int)cudaMemcpyFromSymbol(host, gbm3d::g_tcp_trace, sizeof(long long) * 12 * (n < 4096 ? n : 4096));
 }
 extern "C" int gbm3d_dev_tcp_cnt(long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, gbm3d::g_tcp_cnt, sizeof(long long) * 24 * (n < 4096 ? n : 4096));

@@ -11,12 +11,14 @@ for _ in range(3):
     g.block_match(img, 12, 4, 19, 16, 720000, check=False)
 torch.cuda.synchronize()
 n = 128
-buf = np.zeros((n, 8), np.int64)
+buf = np.zeros((n, 12), np.int64)
 lib.gbm3d_dev_tcp_trace(buf.ctypes.data_as(ctypes.c_void_p), n)
 t0 = buf[:, 0].min()
 b = (buf - t0) / 1000.0
 print("start   spread (us)", b[:, 0].min(), b[:, 0].max())
 print("raw     (us) median", np.median(b[:, 1] - b[:, 0]), "max", (b[:, 1] - b[:, 0]).max())
+print("hs      (us) median", np.median(b[:, 8] - b[:, 0]))
+print("nq      (us) median", np.median(b[:, 9] - b[:, 0]))
 print("prolog  (us) median", np.median(b[:, 2] - b[:, 0]), "max", (b[:, 2] - b[:, 0]).max())
 for w in range(4):
     print(f"warp {w} main (us) median", np.median(b[:, 3 + w] - b[:, 2]), "max", (b[:, 3 + w] - b[:, 2]).max())
