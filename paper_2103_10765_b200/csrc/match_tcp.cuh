@@ -51,9 +51,19 @@ constexpr int XP = XQ * 128;         // bytes per pre-shifted plane row (8 shift
 constexpr int NTS = 5;               // accumulator stages in flight
 constexpr int SPITCH = NB;           // TMEM columns per stage
 constexpr int TM_A = (NTS * SPITCH + 31) / 32 * 32;  // A: 12 K16 steps x 8 columns (two fp16 each)
-constexpr int EPI_WARPS = 4, MMA_WARP = 4, NWARPS = 8, THREADS = 32 * NWARPS;
-constexpr int STG_PITCH = 44;        // floats per lane: the window's <= 11 groups of 4 columns
-                                     // (lane pitch 44 words: conflict-free STS.128)
+#ifndef GBM3D_TCP_NH
+#define GBM3D_TCP_NH 1
+#endif
+// NH warps per TMEM lane quarter, each taking a part of every reference's window columns with
+// its own list (the lists gate each other and are merged at the end).  Dev switch: NH = 2 is
+// correct but slower on c2 (0.110 vs 0.098 ms: both warps scan every column, and they share
+// the SMSP), so NH = 1.
+constexpr int NH = GBM3D_TCP_NH;
+constexpr int EPI_WARPS = 4 * NH, MMA_WARP = EPI_WARPS;
+constexpr int NWARPS = EPI_WARPS + (NH == 1 ? 4 : 1), THREADS = 32 * NWARPS;
+// floats per lane: the window part's <= 11 (NH = 1) / <= 6 (NH = 2) groups of 4 columns (lane
+// pitch 44 / 28 words: conflict-free STS.128)
+constexpr int STG_PITCH = NH == 1 ? 44 : 28;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int MAX_R = 21;            // shared memory bound (see TcpGeom)
 }  // namespace tcp
@@ -73,7 +83,8 @@ struct TcpGeom {
         g.off_raw = g.off_nq + g.NT * NB * 4;                 // int16 plane [PR][PW] / staging
         const int raw = g.PR * PW * 2, stg = EPI_WARPS * 32 * STG_PITCH * 4;
         g.off_bar = g.off_raw + ((raw > stg ? raw : stg) + 15) / 16 * 16;
-        g.total = g.off_bar + 2 * NTS * 8 + 16;               // tfull, tempty; min, max, tmem
+        g.total = g.off_bar + 2 * NTS * 8 + 16 + NH * 128 * 4;  // tfull, tempty; min, max, tmem;
+                                                                // published gates [NH][128]
         return g;
     }
 };
@@ -164,6 +175,8 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
     uint64_t* const tfull = reinterpret_cast<uint64_t*>(sm + g.off_bar);
     uint64_t* const tempty = tfull + NTS;
     int* const misc = reinterpret_cast<int*>(tempty + NTS);  // zmin, zmax, TMEM address
+    volatile uint32_t* const gpub = reinterpret_cast<volatile uint32_t*>(misc + 4);  // [NH][128]
+    for (int i = threadIdx.x; i < NH * 128; i += THREADS) gpub[i] = KEY_INF;
 
     if (threadIdx.x == 0) {
         TCP_TR(0);
@@ -328,7 +341,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
         // (6) A: TMEM lane m = reference m holds its patch, K = 16 i + j (j >= P zero), two fp16
         // per column, read from X (patch row i = the 8 pixels at the reference column and the
         // next P - 8); epilogue warp w writes its lane quarter
-        if (warp < EPI_WARPS) {
+        if (warp < 4) {
             static_assert(P > 8 && P <= 16 && P % 2 == 0, "A rows: one full and one partial 8-pixel chunk");
             const int m = 32 * warp + lane, a = m >> 3, b = m & 7;
             const int col = b * S + r;
@@ -384,8 +397,10 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
             }
         }
     } else if (warp < EPI_WARPS) {
-        // ---------------- warp w: references of TMEM lane quarter w (lane = reference)
-        const int m = 32 * warp + lane, a = m >> 3, b = m & 7;
+        // ---------------- warp w: references of TMEM lane quarter w & 3 (lane = reference),
+        // window part h = w >> 2
+        const int wq = warp & 3, h = warp >> 2;
+        const int m = 32 * wq + lane, a = m >> 3, b = m & 7;
         const int ky = gy0 + a, kx = gx0 + b;
         const bool active = ky < kr1 && kx < p.Rx_reg;
         const int ry = ky * S, rx = kx * S;  // regular grid positions
@@ -396,13 +411,18 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
         const int tdr0 = p.tdr0;
         if (fast) {
             const float Np = nq[(a * S + r) * NB + b * S + r];
-            const int wn = 2 * r + 1;  // window columns (<= 43)
-            const uint64_t wmask = active ? ((1ull << wn) - 1ull) : 0ull;
-            const int nwg = (2 * r) / 4 + 1;  // staged groups of 4 columns: [b, b + nwg) (bS = 4b)
+            const int wn = 2 * r + 1;         // window columns (<= 43)
+            const int nwg = (2 * r) / 4 + 1;  // groups of 4 columns from bS = 4b
+            // this warp's part of the window: columns bS + [klo, khi), groups [b + glo, b + ghi)
+            const int gsplit = (nwg + 1) / 2;
+            const int glo = (NH == 2 && h == 1) ? gsplit : 0;
+            const int ghi = (NH == 2 && h == 0) ? gsplit : nwg;
+            const int klo = 4 * glo, khi = min(wn, 4 * ghi);
+            const uint64_t wmask = active ? (((1ull << khi) - 1ull) & ~((1ull << klo) - 1ull)) : 0ull;
             float* const stg = reinterpret_cast<float*>(sm + g.off_raw) + (32 * warp + lane) * STG_PITCH;
-            float* const stgb = stg - 4 * b;
-            const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
-            const int trow0 = 4 * warp * S, trow1 = (4 * warp + 3) * S + 2 * r;
+            float* const stgb = stg - 4 * (b + glo);
+            const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16);
+            const int trow0 = 4 * wq * S, trow1 = (4 * wq + 3) * S + 2 * r;
             float T = (float)(tdr0 + 1) - Np;
             const int step = nrow > 0 ? row_step(nrow) : 1;
             int s = 0, tc_ = 0;
@@ -426,32 +446,44 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                 return -1;
             };
             uint32_t acc[NB];
+            auto load_acc = [&](int tsx) {
+#pragma unroll
+                for (int c = 0; c < NB / 16; ++c)
+                    tc::tmem_ld16p(taddr + (uint32_t)(tsx * SPITCH + 16 * c), acc + 16 * c);
+            };
+            // the row's candidate norms in registers, loaded with its accumulators (ahead of use)
+            float4 nqv[NB / 4];
+            auto load_nq = [&](int tx) {
+                const float4* nqr = reinterpret_cast<const float4*>(nq + tx * NB);
+#pragma unroll
+                for (int c = 0; c < NB / 4; ++c) nqv[c] = nqr[c];
+            };
             int ts = 0;
             int t = next_row(ts);
             if (t >= 0) {
-#pragma unroll
-                for (int c = 0; c < NB / 16; ++c)
-                    tc::tmem_ld16p(taddr + (uint32_t)(ts * SPITCH + 16 * c), acc + 16 * c);
+                load_acc(ts);
+                load_nq(t);
             }
             while (t >= 0) {
+                long long k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+                (void)k0; (void)k1; (void)k2; (void)k3;
+                TCP_CLK(k0);
                 tc::tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < NB / 16; ++c) tc::tmem_tie16(acc + 16 * c);
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&tempty[ts]);
-                // u = N_q - 2 <f_p, f_q> (exact for every passing candidate); the lane's window
-                // groups staged; pass bits = sign of u - T, bit j of word j / 32
-                const float* nqr = nq + t * NB;
+                // u = N_q - 2 <f_p, f_q> (exact for every passing candidate); the lane's groups
+                // staged; pass bits = sign of u - T, bit j of word j / 32
                 uint32_t mk[3] = {0u, 0u, 0u};
 #pragma unroll
                 for (int c = NB / 4 - 1; c >= 0; --c) {
-                    const float4 n4 = *reinterpret_cast<const float4*>(nqr + 4 * c);
-                    const float nv[4] = {n4.x, n4.y, n4.z, n4.w};
+                    const float nv[4] = {nqv[c].x, nqv[c].y, nqv[c].z, nqv[c].w};
                     float u[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) u[e] = fmaf(-2.f, __uint_as_float(acc[4 * c + e]), nv[e]);
-                    if ((unsigned)(c - b) < (unsigned)nwg)
+                    if ((unsigned)(c - b - glo) < (unsigned)(ghi - glo))
                         *reinterpret_cast<float4*>(stgb + 4 * c) = make_float4(u[0], u[1], u[2], u[3]);
 #pragma unroll
                     for (int e = 3; e >= 0; --e) {
@@ -466,19 +498,21 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                 if (bs > 0) mw |= (uint64_t)mk[2] << (64 - bs);
                 mw &= ((unsigned)tt <= (unsigned)(2 * r)) ? wmask : 0ull;
                 if (tt == r) mw &= ~(1ull << r);  // the reference itself (slot 0)
+                TCP_CLK(k1);
                 // the next row's accumulators load while this row's keys are inserted
                 int tsn = 0;
                 const int tn = next_row(tsn);
                 if (tn >= 0) {
-#pragma unroll
-                    for (int c = 0; c < NB / 16; ++c)
-                        tc::tmem_ld16p(taddr + (uint32_t)(tsn * SPITCH + 16 * c), acc + 16 * c);
+                    load_acc(tsn);
+                    load_nq(tn);
                 }
+                TCP_CLK(k2);
                 const uint32_t cbase = (uint32_t)(tt * p.side);
                 auto pop = [&]() -> uint32_t {
                     const int j = __ffsll((long long)mw) - 1;
                     mw &= mw - 1ull;
-                    const uint32_t key = (__float2uint_rn(stg[max(j, 0)] + Np) << cb) | (cbase + (uint32_t)j);
+                    const uint32_t key =
+                        (__float2uint_rn(stg[max(j - klo, 0)] + Np) << cb) | (cbase + (uint32_t)j);
                     return j >= 0 ? key : KEY_INF;
                 };
                 int nr_ = 0;
@@ -490,14 +524,42 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                     const uint32_t k1 = pop(), k2 = pop();
                     ins2<KL>(L, min(k1, k2), max(k1, k2));
                 }
+                TCP_CLK(k3);
+                TCP_ADD(0, k2 - k1);
+                TCP_ADD(1, k1 - k0);
+                TCP_ADD(2, k3 - k2);
                 TCP_ADD(3, nr_);
                 TCP_ADD(4, 1);
-                const int gd = min((int)(L[KL - 1] >> cb), tdr0);
+                // gate: the (K-1)-th key of this list or of the partner's (either bounds the
+                // union's (K-1)-th)
+                uint32_t gk = L[KL - 1];
+                if (NH == 2) {
+                    gpub[h * 128 + m] = gk;
+                    gk = min(gk, gpub[(1 - h) * 128 + m]);
+                }
+                const int gd = min((int)(gk >> cb), tdr0);
                 T = (float)(gd + 1) - Np;
                 t = tn;
                 ts = tsn;
             }
-        } else if (active) {
+            if (NH == 2) {
+                // merge: part 1 hands its list over (X is free: every MMA has completed), part 0
+                // inserts the partner's K - 1 real keys
+                uint32_t* const mb = reinterpret_cast<uint32_t*>(sm + g.off_x);
+                if (h == 1) {
+#pragma unroll
+                    for (int i = 0; i < KL; ++i) mb[i * 128 + m] = L[i];
+                }
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+                if (h == 0) {
+                    for (int i = nfill; i < KL; i += 2) {
+                        const uint32_t lo = mb[i * 128 + m], hi = i + 1 < KL ? mb[(i + 1) * 128 + m] : KEY_INF;
+                        if (!__any_sync(0xffffffffu, lo < L[KL - 1])) break;
+                        ins2<KL>(L, lo, hi);
+                    }
+                }
+            }
+        } else if (active && h == 0) {
             // ---------------- exact int32 path for a tile above the fp16 bound: direct Eq. (1)
             const int pa = a * S + r, pb = b * S + r;  // the reference's plane position
             for (int dy = -r; dy <= r; ++dy) {
@@ -521,9 +583,9 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                 }
             }
         }
-        if (lane == 0) TCP_TR(3 + warp);
-        // ---------------- output: slot 0 = self, ranks 1 .. K-1, pads (self, -1)
-        if (active) {
+        if (lane == 0 && warp < 4) TCP_TR(3 + warp);
+        // ---------------- output (part 0): slot 0 = self, ranks 1 .. K-1, pads (self, -1)
+        if (active && h == 0) {
             const int self = ry * p.W + rx;
             const int64_t ref = (int64_t)bimg * p.out_bstride + (int64_t)(ky - p.row_begin) * p.Rx + kx;
             int32_t* const oi = p.idx + ref * p.K;
