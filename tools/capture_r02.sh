@@ -15,3 +15,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:matc
 timeout 120 python tools/run_once.py --config c4 > gpurun_out/plain_c4.log 2>&1 &&
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:match_tc16 -c 1 \
    -o gpurun_out/prof_c4 -f python tools/run_once.py --config c4 > gpurun_out/ncu_full4.log 2>&1; echo "ncu c4 rc=$?"
+timeout 120 python tools/run_once.py --config c2 > gpurun_out/plain_c2.log 2>&1 &&
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:match_tcp -c 1 \
+   -o gpurun_out/prof_c2 -f python tools/run_once.py --config c2 > gpurun_out/ncu_full2.log 2>&1; echo "ncu c2 rc=$?"
