@@ -318,6 +318,27 @@ def test_row_ranges_concatenate_to_full(cuts):
         assert torch.equal(torch.cat([p[i] for p in parts]), full[i])
 
 
+@pytest.mark.parametrize("cuts", [[17], [5, 40, 41]])
+def test_row_ranges_p12_product(cuts):
+    """Row-range calls (emulated shards with halo slabs) through the patch-12 tensor-core kernel:
+    tiles start at the call's first row and read only the slab; the concatenation equals the
+    oracle's full table."""
+    g = _gbm3d()
+    img = config_images("c2")[0][:230, :150].copy()
+    H, W, P, s, r, K, tau = 230, 150, 12, 4, 19, 16, 720000
+    Ry, Rx = g.grid_dims(H, W, P, s)
+    splits = [0] + cuts + [Ry]
+    parts = []
+    for a, b in zip(splits[:-1], splits[1:]):
+        y0 = min(a * s, H - P)
+        ylast = min(min(b - 1, Ry - 1) * s, H - P)
+        lo, hi = max(0, y0 - r), min(H, ylast + r + P)
+        slab = torch.from_numpy(img[lo:hi].copy()).cuda()
+        parts.append([t.cpu().numpy() for t in g.block_match_rows(slab, lo, H, W, P, s, r, K, tau, a, b)])
+    got = tuple(np.concatenate([p[i] for p in parts]) for i in range(3))
+    _assert_same(got, oracle.block_match(img, P, s, r, K, tau), f"P12 rows {cuts}")
+
+
 def test_rows_rejects_short_slab():
     g = _gbm3d()
     img = torch.zeros((100, 64), dtype=torch.int16, device="cuda")

@@ -10,7 +10,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 bid = open(sys.argv[1]).read().split("src ")[-1].strip()
 out = {"build": bid, "source": "ncu --set full --clock-control none, one launch of the step's "
-                                "dominant kernel (match_tc16), tools/capture_r02.sh"}
+                                "dominant kernel (match_tc16 for c3 / c4, match_tcp for c2), "
+                                "tools/capture_r02.sh"}
 keep = ("kernel", "duration_s", "dram_bytes", "dram_gbs", "alu_pipe_pct", "fma_pipe_pct",
         "lsu_pipe_pct", "issue_active_pct", "ipc_active", "inst_executed", "sm_clock_hz",
         "shared_wavefronts", "shared_bank_conflicts", "shared_gbs_upper", "shared_pipe_pct",
