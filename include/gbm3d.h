@@ -22,9 +22,9 @@
  *     tile-centred pixels, fp32 accumulators; every partial sum is an integer below 2^24, so
  *     exact; tiles whose pixel range breaks that bound are redone by an int8 byte-plane
  *     kernel), norms by box sums (step 1); likewise patch 12 / stride 4 /
- *     radius <= 21 / K <= 32 when tau - 1 <= 2^(32 - cb) - 1 (the 32-bit key's d range; c2):
- *     12 MMAs of K16 per candidate row, tiles above the fp16 bound take an in-kernel exact
- *     int32 path;
+ *     radius <= 21 / K <= 32 (c2): 12 MMAs of K16 per candidate row, tiles above the fp16
+ *     bound and references whose 32-bit-key lists end short (tau - 1 above the key's d
+ *     range) take in-kernel exact int32 paths;
  *   - SSD form, organised by displacement delta = c - rho: the shifted-difference image
  *     (Z - S_delta Z)^2 box-summed over P x P (Prop. 1 with an all-ones block,
  *     PAPER.md:89-113), in int32; used for the other instantiated shapes.

@@ -58,11 +58,11 @@ extern template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream
 static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok,
                                bool int8_only) {
     *ok = false;
-    // patch 12 / stride 4 (c2): fp16 product form with an in-kernel exact path for tiles above
-    // the fp16 bound; needs tau - 1 <= dsat (every listed key exact) and the tile's columns
-    // 7S + 2r + 1 <= 80 within the shared-memory bound (radius <= 21)
+    // patch 12 / stride 4 (c2): fp16 product form with in-kernel exact paths (tiles above the
+    // fp16 bound; references whose 32-bit-key lists end short when tau - 1 > dsat); the tile's
+    // columns 7S + 2r + 1 <= 80 within the shared-memory bound (radius <= 21)
     if (p.P == 12 && p.S == 4 && !int8_only && p.r <= tcp::MAX_R && 7 * p.S + 2 * p.r + 1 <= tcp::NB &&
-        p.K >= 2 && p.K <= 32 && !p.tau_above_dsat) {
+        p.K >= 2 && p.K <= 32) {
         *ok = true;
         if (p.K - 1 <= 15) return launch_tcp<12, 4, 15>(p, st, launches);
         return launch_tcp<12, 4, 31>(p, st, launches);

@@ -29,8 +29,9 @@
 //   * Candidate rows are visited in a scrambled order (t = t_lo + s * step mod n, step coprime to
 //     n near 0.618 n) so that every warp has work in every stretch of rows and the lists fill
 //     with typical distances early.
-//   * Keys are exact because the call's tau satisfies tau - 1 <= dsat (the dispatcher's
-//     condition): a candidate with d > tau - 1 never enters a list.
+//   * Keys are exact while d <= dsat = 2^(32 - cb) - 1: the gate starts at min(dsat, tau - 1), so a
+//     candidate with larger d never enters a list; when tau - 1 > dsat, a reference whose list
+//     ends short is recomputed exactly with 64-bit keys (direct Eq. (1) from the tile's pixels).
 #pragma once
 #include <cuda_fp16.h>
 
@@ -127,8 +128,8 @@ static __device__ __forceinline__ void ins2(uint32_t (&L)[KL], uint32_t lo, uint
     if (KL >= 2) L[1] = min(L[1], min(max(L[0], lo), hi));
     L[0] = min(L[0], lo);
 }
-template <int KL>
-static __device__ __forceinline__ void ins1(uint32_t (&L)[KL], uint32_t x) {
+template <int KL, typename KT>
+static __device__ __forceinline__ void ins1(KT (&L)[KL], KT x) {
 #pragma unroll
     for (int k = KL - 1; k >= 1; --k) L[k] = min(L[k], max(L[k - 1], x));
     L[0] = min(L[0], x);
@@ -543,9 +544,10 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                 ts = tsn;
             }
             if (NH == 2) {
-                // merge: part 1 hands its list over (X is free: every MMA has completed), part 0
-                // inserts the partner's K - 1 real keys
-                uint32_t* const mb = reinterpret_cast<uint32_t*>(sm + g.off_x);
+                // merge: part 1 hands its list over (through the norms' buffer, dead once every
+                // row is scanned; X stays intact), part 0 inserts the partner's K - 1 real keys
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * EPI_WARPS) : "memory");
+                uint32_t* const mb = reinterpret_cast<uint32_t*>(sm + g.off_nq);
                 if (h == 1) {
 #pragma unroll
                     for (int i = 0; i < KL; ++i) mb[i * 128 + m] = L[i];
@@ -579,7 +581,47 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
                         }
                     }
                     if (d <= tdr0)
-                        ins1<KL>(L, ((uint32_t)d << cb) | (uint32_t)((dy + r) * p.side + dx + r));
+                        ins1<KL, uint32_t>(L, ((uint32_t)d << cb) | (uint32_t)((dy + r) * p.side + dx + r));
+                }
+            }
+        }
+        // ---------------- tau - 1 above the 32-bit key's d range (dsat): keys stop at d <= dsat,
+        // so a list that ended short may miss valid candidates with larger d; such a reference
+        // is recomputed exactly (direct Eq. (1) in int32, 64-bit keys d << 32 | code) from the
+        // pixels still in shared memory (X in the fp16 path, the int16 plane otherwise)
+        bool exact64 = false;
+        uint64_t L64[KL];
+        if (p.tau_above_dsat && active && h == 0) {
+            int nreal = 0;
+#pragma unroll
+            for (int i = 0; i < KL; ++i) nreal += (i >= nfill && L[i] != KEY_INF) ? 1 : 0;
+            if (nreal < p.K - 1) {
+                exact64 = true;
+#pragma unroll
+                for (int i = 0; i < KL; ++i) L64[i] = i < nfill ? 0ull : ~0ull;
+                const int pa = a * S + r, pb = b * S + r;
+                auto pix = [&](int y, int x) -> int {
+                    if (fast)
+                        return __half2int_rn(*reinterpret_cast<const __half*>(
+                            sm + g.off_x + y * XP + (x >> 3) * 128 + (x & 7) * 16));
+                    return (int)raw[y * PW + x];
+                };
+                for (int dy = -r; dy <= r; ++dy) {
+                    const int cy = ry + dy;
+                    if (cy < ylo || cy > yhi - P) continue;
+                    for (int dx = -r; dx <= r; ++dx) {
+                        const int cx = rx + dx;
+                        if (cx < 0 || cx > p.W - P || (dy == 0 && dx == 0)) continue;
+                        int d = 0;
+                        for (int i = 0; i < P; ++i)
+                            for (int jj = 0; jj < P; ++jj) {
+                                const int df = pix(pa + i, pb + jj) - pix(pa + dy + i, pb + dx + jj);
+                                d += df * df;
+                            }
+                        if ((int64_t)d < p.tau)
+                            ins1<KL, uint64_t>(L64, ((uint64_t)(uint32_t)d << 32) |
+                                                        (uint64_t)((dy + r) * p.side + dx + r));
+                    }
                 }
             }
         }
@@ -598,12 +640,12 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
             for (int i = 0; i < KL; ++i) {
                 const int s = i - nfill + 1;
                 if (s >= 1) {
-                    const uint32_t key = L[i];
-                    if (key != KEY_INF) {
-                        const int code = (int)(key & cmask);
+                    const bool valid = exact64 ? L64[i] != ~0ull : L[i] != KEY_INF;
+                    if (valid) {
+                        const int code = exact64 ? (int)(uint32_t)L64[i] : (int)(L[i] & cmask);
                         const int dy = code / p.side - r, dx = code - (code / p.side) * p.side - r;
                         oi[s] = (ry + dy) * p.W + rx + dx;
-                        od[s] = (int)(key >> cb);
+                        od[s] = exact64 ? (int)(L64[i] >> 32) : (int)(L[i] >> cb);
                         ++cnt;
                     } else {
                         oi[s] = self;

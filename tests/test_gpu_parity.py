@@ -53,7 +53,7 @@ def _product_supported(P, s, r, K, tau=None, method="product"):
     if P == 8 and s == 3:
         return 7 * s + 2 * r + 1 <= 64 and 2 <= K <= 32
     if P == 12 and s == 4 and method == "product":
-        return r <= 21 and 2 <= K <= 32 and tau is not None and tau - 1 <= (1 << 21) - 1
+        return r <= 21 and 2 <= K <= 32
     return False
 
 
@@ -157,8 +157,6 @@ def test_product_mixed_range_tiles():
 def test_product_unsupported_shape_reports():
     g = _gbm3d()
     img = torch.from_numpy(config_images("c2")[0]).cuda()
-    with pytest.raises(g.GBM3DError):   # P12 without tau: keys beyond the 32-bit d range
-        g.block_match(img, 12, 4, 19, 16, None, method="product")
     with pytest.raises(g.GBM3DError):   # no int8 kernel for P12
         g.block_match(img, 12, 4, 19, 16, 720000, method="product_i8")
     with pytest.raises(g.GBM3DError):   # radius above the P12 shared-memory bound
@@ -189,6 +187,19 @@ def test_p12_product_edge_cases(H, W, r, K, tau, kind):
     exp = oracle.block_match(img, 12, 4, r, K, tau)
     _assert_same(_gpu(img, 12, 4, r, K, tau, method="product"), exp, f"P12 {kind} {H}x{W} r{r} K{K}")
     _assert_same(_gpu(img, 12, 4, r, K, tau), exp, f"P12 auto {kind} {H}x{W} r{r} K{K}")
+
+
+@pytest.mark.parametrize("tau", [None, 1 << 33, 2097153])
+def test_p12_product_above_key_range(tau):
+    """tau - 1 above the 32-bit key's d range (2^21 - 1 at r <= 22): references whose lists end
+    short (high-contrast tiles where fewer than K - 1 candidates have d <= 2^21 - 1) are
+    recomputed exactly with 64-bit keys, in the fp16 path and in the exact int32 path."""
+    rng = np.random.default_rng(11)
+    img = rng.integers(-60, 300, size=(120, 140)).astype(np.int16)      # d ~ 144 * 2 * 10^4 > 2^21
+    img[40:80, 30:100] = rng.integers(0, 12, size=(40, 70)).astype(np.int16)  # lists that fill
+    exp = oracle.block_match(img, 12, 4, 19, 16, tau)
+    _assert_same(_gpu(img, 12, 4, 19, 16, tau, method="product"), exp, f"P12 tau {tau}")
+    _assert_same(_gpu(img, 12, 4, 19, 16, tau), exp, f"P12 auto tau {tau}")
 
 
 @pytest.mark.parametrize("H,W,r,K,tau,sigma,seed", [
@@ -225,7 +236,7 @@ rng = np.random.default_rng(3)
 img2 = rng.integers(-100, 356, size=(150, 170)).astype(np.int16)
 img2[60:110, 20:90] = rng.choice(np.array([-900, 900], np.int16), size=(50, 70))
 out = []
-for im, tau in ((img, 720000), (img2, 2000000)):
+for im, tau in ((img, 720000), (img2, 2000000), (img2, None)):
     i, d, n = g.block_match(torch.from_numpy(im).cuda(), 12, 4, 19, 16, tau, method="product")
     out.append([i.cpu().numpy().tolist(), d.cpu().numpy().tolist(), n.cpu().numpy().tolist()])
 json.dump(out, sys.stdout)
@@ -233,7 +244,7 @@ json.dump(out, sys.stdout)
     rng = np.random.default_rng(3)
     img2 = rng.integers(-100, 356, size=(150, 170)).astype(np.int16)
     img2[60:110, 20:90] = rng.choice(np.array([-900, 900], np.int16), size=(50, 70))
-    cases = ((config_images("c2")[0][:200, :180].copy(), 720000), (img2, 2000000))
+    cases = ((config_images("c2")[0][:200, :180].copy(), 720000), (img2, 2000000), (img2, None))
     for mmax in ("0", None):
         env = dict(os.environ)
         if mmax is not None:
