@@ -641,6 +641,9 @@ def main():
     ap.add_argument("--method", default="auto", choices=["auto", "ssd", "product", "direct"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-also", action="store_true", help="skip the secondary c4 line")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N > 1, c3: tables to rank 0 by peer stores from the matcher into "
+                         "symmetric memory (default) or by the chunked NCCL gather")
     ap.add_argument("--step-only", action="store_true",
                     help="only the timed matching step (no gather / stage legs, e2e, CPU "
                          "baseline): for ncu launch lists of the step")

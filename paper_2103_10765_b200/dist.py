@@ -225,6 +225,54 @@ def block_match_rowsharded(img_rows: torch.Tensor, slab_y0: int, H: int, W: int,
     return full
 
 
+# --------------------------------------------------------------- peer stores (symmetric memory)
+class PeerTables:
+    """Row-sharded output tables in symmetric memory: the gather fused into the matcher.
+
+    Every rank allocates the same buffer (idx, dist [Ry, Rx, K] and n_valid [Ry, Rx], one int32
+    allocation) with torch's symmetric memory and rendezvouses; ``dst_views`` are views of rank
+    ``dst``'s buffer mapped into this rank's address space (NVLink peer memory on the box).  Each
+    rank's matching kernel is handed those views as its output pointers, so its 16-byte result
+    stores travel straight to rank ``dst`` tile by tile while the next tiles are matched -- no
+    separate gather, no staging copy.  ``finish`` is the stream-ordered device barrier of the
+    symmetric-memory handle: after it, rank ``dst`` sees every rank's rows.  ``tables`` on rank
+    ``dst`` are the full tables."""
+
+    def __init__(self, Ry: int, Rx: int, K: int, dev, dst: int = 0, group=None):
+        import torch.distributed._symmetric_memory as symm
+        grp = group if group is not None else dist.group.WORLD
+        n = Ry * Rx * (2 * K + 1)
+        self.buf = symm.empty(n, dtype=torch.int32, device=dev)
+        try:
+            self.hdl = symm.rendezvous(self.buf, grp)
+        except RuntimeError:
+            symm.enable_symm_mem_for_group(grp.group_name)
+            self.hdl = symm.rendezvous(self.buf, grp)
+        peer = self.hdl.get_buffer(dst, (n,), torch.int32)
+        t = Ry * Rx * K
+        self.dst_views = (peer[:t].view(Ry, Rx, K), peer[t:2 * t].view(Ry, Rx, K),
+                          peer[2 * t:].view(Ry, Rx))
+        self.tables = (self.buf[:t].view(Ry, Rx, K), self.buf[t:2 * t].view(Ry, Rx, K),
+                       self.buf[2 * t:].view(Ry, Rx))
+
+    def rows(self, a: int, b: int):
+        """Output views of global reference rows [a, b) in rank ``dst``'s tables."""
+        return tuple(v[a:b] for v in self.dst_views)
+
+    def finish(self):
+        self.hdl.barrier(channel=0)
+
+
+def _peer_step(g, cfg, call, slab, y0, ranges, rank, peer: PeerTables):
+    """One row-sharded step with the gather fused into the matcher: this rank's rows are matched
+    straight into rank 0's tables (peer stores), then the device barrier."""
+    k0, k1 = ranges[rank]
+    if k1 > k0:
+        g.block_match_rows(slab, y0, cfg.H, cfg.W, call.patch, call.stride, call.radius, call.K,
+                           call.tau, k0, k1, out=peer.rows(k0, k1))
+    peer.finish()
+
+
 # ------------------------------------------------------------------------------ bench (N > 1)
 def _init():
     if not dist.is_initialized():
@@ -324,8 +372,9 @@ def _e2e_multi(args, cfg, call, g, dev, rank, world, sharded):
 
 
 def bench_multi(args, cfg, call, sampler=None):
-    """N-GPU measurement: c3 row-sharded + NCCL gather to rank 0 (timed), c4 batch split
-    (no collective).  Max over ranks of the per-rank device time.  `sampler` (optional, with
+    """N-GPU measurement: c3 row-sharded with the tables gathered on rank 0 (timed; by default
+    the matcher stores its rows straight into rank 0's symmetric-memory tables, `PeerTables`;
+    `--gather nccl` = the chunked NCCL gather), c4 batch split (no collective).  Max over ranks of the per-rank device time.  `sampler` (optional, with
     start() / stop() / summary()) samples this rank's GPU clocks around the timed region; rank
     0 reports the lowest median clock and the union of throttle reasons over the ranks.  The
     end-to-end leg times, per step and on every rank, the pinned-host copy of the rank's input
@@ -354,11 +403,25 @@ def bench_multi(args, cfg, call, sampler=None):
                     torch.empty((Ry, Rx, call.K), dtype=torch.int32, device=dev),
                     torch.empty((Ry, Rx), dtype=torch.int32, device=dev))
         streams = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
+        # the gather: fused into the matcher as peer stores to rank 0's symmetric-memory tables
+        # (default), else the chunked NCCL point-to-point gather overlapped with the matching
+        peer = None
+        gather_mode = getattr(args, "gather", "peer")
+        if gather_mode == "peer":
+            try:
+                peer = PeerTables(Ry, Rx, call.K, dev)
+            except Exception as e:  # no symmetric memory on this stack: the NCCL gather
+                gather_mode = f"nccl (peer stores unavailable: {type(e).__name__})"
 
         def step():
-            _sharded_step(g, cfg, call, slab, y0, ranges, rank, world, local_out, full, streams)
+            if peer is not None:
+                _peer_step(g, cfg, call, slab, y0, ranges, rank, peer)
+            else:
+                _sharded_step(g, cfg, call, slab, y0, ranges, rank, world, local_out, full,
+                              streams)
         my_refs = (k1 - k0) * Rx
     else:
+        gather_mode = None
         ranges = batch_partition(cfg.B, world)
         b0, b1 = ranges[rank]
         imgs = torch.from_numpy(config_images(cfg)[b0:b1]).to(dev)
@@ -416,8 +479,11 @@ def bench_multi(args, cfg, call, sampler=None):
                 "config": {"workload": f"{cfg.name}: {cfg.note}", "H": cfg.H, "W": cfg.W,
                            "B": cfg.B, "patch": call.patch, "stride": call.stride,
                            "radius": call.radius, "K": call.K, "tau": call.tau,
-                           "parallelism": ("rows+nccl-gather" if sharded else "batch") +
-                           f"x{world}", "l2": "256 MiB write between timed steps"},
+                           "parallelism": ("rows+" + ("peer-store-gather" if peer is not None
+                                                      else "nccl-gather")
+                                           if sharded else "batch") + f"x{world}",
+                           "l2": "256 MiB write between timed steps"},
+                "table_gather": gather_mode,
                 "gpu_launches": launches * args.steps,
                 "rank0_refs": my_refs}
         if e2e_ms is not None:

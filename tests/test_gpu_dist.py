@@ -48,3 +48,37 @@ def test_chunked_sharded_pipeline_single_rank():
             assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_store_tables_single_rank():
+    """The fused gather: PeerTables allocates the tables in torch symmetric memory, the matcher
+    writes its rows through the views of rank 0's buffer (here the rank itself), and after the
+    device barrier the tables equal one whole-image call bit for bit (two steps, the second
+    over stale contents)."""
+    import torch.distributed as dist
+
+    import paper_2103_10765_b200 as g
+    from paper_2103_10765_b200 import dist as gd
+    from synth import CONFIGS, config_images
+    cfg = CONFIGS["c3"]
+    call = cfg.calls[0]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        img = torch.from_numpy(config_images(cfg)[0]).to(dev)
+        Ry, Rx = g.grid_dims(cfg.H, cfg.W, call.patch, call.stride)
+        ranges = gd.row_partition(Ry, 1, gd.TILE_ROWS)
+        peer = gd.PeerTables(Ry, Rx, call.K, dev)
+        peer.buf.fill_(-7)
+        ref = g.block_match(img, call.patch, call.stride, call.radius, call.K, call.tau)
+        for _ in range(2):
+            gd._peer_step(g, cfg, call, img, 0, ranges, 0, peer)
+            torch.cuda.synchronize()
+            for a, b in zip(peer.tables, ref):
+                assert torch.equal(a, b)
+            peer.buf.fill_(-7)
+    finally:
+        dist.destroy_process_group()
