@@ -126,7 +126,11 @@ static cudaError_t launch_direct(const MatchParams& p, cudaStream_t st, int k_be
               : p.P == 16 ? match_direct_kernel<16> : match_direct_kernel<0>;
     const long long nref = (long long)(k_end - k_begin) * (m_end - m_begin);
     dim3 grid((unsigned)nref, 1, p.B);
-    kern<<<grid, DIRECT_THREADS, 0, st>>>(p, k_begin, m_begin, m_end - m_begin);
+    // one thread per task of 8 candidates of a full window (rounded to warps, 64..256): no
+    // idle warps for small windows (P16 r16: 33 x 5 tasks -> 192 threads)
+    const int side = 2 * p.r + 1, ntask = side * ((side + DIRECT_CG - 1) / DIRECT_CG);
+    const int nthr = std::max(64, std::min(DIRECT_THREADS, (ntask + 31) / 32 * 32));
+    kern<<<grid, nthr, 0, st>>>(p, k_begin, m_begin, m_end - m_begin);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
