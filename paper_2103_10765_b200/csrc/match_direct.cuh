@@ -25,13 +25,63 @@ constexpr int DIRECT_WIN = DIRECT_ROWS + DIRECT_CG;  // int32 row pitch (+ zero 
 // top-left pixels are window columns x .. x + 7 of window row y (win: shared int32, pitch
 // DIRECT_WIN, 16-byte aligned rows; x a multiple of 8).  Per patch row: 16-byte loads of the
 // P + 7 window pixels and of the reference row (a broadcast), then 8 P ISUB + IMAD.
+//
+// Compile-time patch 12 or 16: Eq. (2), d = ||f_p||^2 + ||f_q||^2 - 2 <f_p, f_q>,
+// in uint32 arithmetic modulo 2^32 -- one IMAD per pixel pair for the inner products, the
+// candidates' norms from sliding row sums of the squared window row (P + 7 squares and 2 ops
+// per candidate per row) -- instead of ISUB + IMAD per pair.  Exact: the true d is < 2^31
+// (range precondition R10), so the wrapped value is d.  `np` = ||f_p||^2 mod 2^32.  (At P = 8
+// the saving per row is smaller than the longer dependency chains cost: 1.76 -> 1.87 ms.)
 template <int PT>
 static __device__ __forceinline__ void direct_ssd8(const int* __restrict__ ref,
                                                    const int* __restrict__ win, int P, int y,
-                                                   int x, int (&acc)[DIRECT_CG]) {
+                                                   int x, int (&acc)[DIRECT_CG], uint32_t np) {
     constexpr int PM = PT > 0 ? PT : 16;
     constexpr int NW = (PM + DIRECT_CG - 1 + 3) / 4;  // 16-byte window loads per row
     const int Pn = PT > 0 ? PT : P;
+    if (PT >= 12) {
+        uint32_t ip[DIRECT_CG], nq[DIRECT_CG];
+#pragma unroll
+        for (int c = 0; c < DIRECT_CG; ++c) ip[c] = nq[c] = 0u;
+#pragma unroll 1
+        for (int i = 0; i < PM; ++i) {
+            const int4* row = reinterpret_cast<const int4*>(win + (y + i) * DIRECT_WIN + x);
+            uint32_t w[4 * NW];
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                const int4 v = row[q];
+                w[4 * q] = (uint32_t)v.x;
+                w[4 * q + 1] = (uint32_t)v.y;
+                w[4 * q + 2] = (uint32_t)v.z;
+                w[4 * q + 3] = (uint32_t)v.w;
+            }
+            const int4* rr = reinterpret_cast<const int4*>(ref + i * 16);
+#pragma unroll
+            for (int q = 0; q < PM / 4; ++q) {
+                const int4 a4 = rr[q];
+                const uint32_t av[4] = {(uint32_t)a4.x, (uint32_t)a4.y, (uint32_t)a4.z, (uint32_t)a4.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int c = 0; c < DIRECT_CG; ++c) ip[c] += av[jj] * w[c + 4 * q + jj];
+            }
+            uint32_t sq[PM + DIRECT_CG - 1];
+#pragma unroll
+            for (int k = 0; k < PM + DIRECT_CG - 1; ++k) sq[k] = w[k] * w[k];
+            uint32_t rs = 0u;
+#pragma unroll
+            for (int k = 0; k < PM; ++k) rs += sq[k];
+            nq[0] += rs;
+#pragma unroll
+            for (int c = 1; c < DIRECT_CG; ++c) {
+                rs += sq[c + PM - 1] - sq[c - 1];
+                nq[c] += rs;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < DIRECT_CG; ++c) acc[c] = (int)(np + nq[c] - 2u * ip[c]);
+        return;
+    }
 #pragma unroll 1
     for (int i = 0; i < Pn; ++i) {
         const int4* row = reinterpret_cast<const int4*>(win + (y + i) * DIRECT_WIN + x);
@@ -153,7 +203,21 @@ __global__ void __launch_bounds__(DIRECT_THREADS) match_direct_kernel(MatchParam
     }
     for (int i = threadIdx.x; i < P * P; i += blockDim.x)
         refpatch[(i / P) * 16 + i % P] = img[(int64_t)(ry + i / P - p.slab_y0) * W + rx + i % P];
+    __shared__ uint32_t s_np;  // ||f_p||^2 mod 2^32 (Eq. (2) path)
+    if (threadIdx.x == 0) s_np = 0u;
     __syncthreads();
+    if (PT >= 12) {
+        uint32_t v = 0u;
+        for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
+            const uint32_t z = (uint32_t)refpatch[(i / P) * 16 + i % P];
+            v += z * z;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) atomicAdd(&s_np, v);
+        __syncthreads();
+    }
+    const uint32_t np = s_np;
     // every warp: tasks of 8 candidates along x, then one selection round per candidate slot
     // (keys (d << 32 | idx); INF for d >= tau, the reference itself and the padding)
     dkey q0 = ~0ull, q1 = ~0ull;
@@ -166,7 +230,7 @@ __global__ void __launch_bounds__(DIRECT_THREADS) match_direct_kernel(MatchParam
         if (task < ntask) {
             const int yy = task / gx, x8 = DIRECT_CG * (task - yy * gx);
             int acc[DIRECT_CG] = {0, 0, 0, 0, 0, 0, 0, 0};
-            direct_ssd8<PT>(refpatch, win, P, yy, x8, acc);
+            direct_ssd8<PT>(refpatch, win, P, yy, x8, acc, np);
 #pragma unroll
             for (int c = 0; c < DIRECT_CG; ++c) {
                 const int cy = cy0 + yy, cx = cx0 + x8 + c;
