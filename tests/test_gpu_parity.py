@@ -480,3 +480,31 @@ def test_cuda_graph_replay_matches_oracle(name, ci):
     got = tuple(o.cpu().numpy() for o in outs)
     _assert_same(got, oracle.block_match(img2, c.patch, c.stride, c.radius, c.K, c.tau),
                  f"graph replay {name} call {ci}")
+
+
+def test_fuzz_p12_and_direct_p16():
+    """60 random cases on the round's new paths: the patch-12 tensor-core kernel (r <= 21 incl.
+    the 64-bit recompute when tau - 1 exceeds the 32-bit key range, r > 21 on the strip
+    kernel) and the direct kernel's modular Eq. (2) form at P 12 / 16 (strides with no fast
+    kernel), natural-looking and uniform images, single and batched, bit-exact vs the oracle."""
+    from synth import make_image
+    rng = np.random.default_rng(77)
+    g = _gbm3d()
+    for case in range(60):
+        P, s = [(12, 4), (12, 4), (12, 4), (16, 16), (12, 13), (16, 5)][case % 6]
+        H = int(rng.integers(P, 130))
+        W = int(rng.integers(P, 130))
+        r = int(rng.integers(0, 26))
+        K = int(rng.integers(1, 40))
+        tau = [None, int(rng.integers(0, 1500000)), int(rng.integers(0, 1 << 33))][case % 3]
+        if case % 2:
+            img = make_image(H, W, 6, 2, float(rng.uniform(5, 50)), case + 500)
+        else:
+            img = special_image("uniform", H, W, seed=case + 500, lo=-150, hi=400)
+        what = f"p12/p16 fuzz {case}: {H}x{W} P{P} s{s} r{r} K{K} tau{tau}"
+        _assert_same(_gpu(img, P, s, r, K, tau), oracle.block_match(img, P, s, r, K, tau), what)
+        if case % 10 == 0:
+            imgs = np.stack([img, np.ascontiguousarray(img[::-1])])
+            i, d, n = g.block_match(torch.from_numpy(imgs).cuda(), P, s, r, K, tau)
+            _assert_same((i.cpu().numpy(), d.cpu().numpy(), n.cpu().numpy()),
+                         oracle.block_match_batched(imgs, P, s, r, K, tau), what + " batched")
