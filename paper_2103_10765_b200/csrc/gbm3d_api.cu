@@ -173,10 +173,27 @@ static SideStreams* side_for_current_device() {
     return sd->init() ? sd : nullptr;
 }
 
+// AUTO on tiny jobs (latency cases): the tile kernels need about one tile's time on
+// one SM however few references there are (c0: 68 us), while the per-reference direct kernel
+// spreads the references over every SM (c0: 26 us).  Below this much pixel work (references x
+// window x patch^2) the direct kernel is faster (c0 3.9e7: direct; c1 6.9e8: tile kernels).
+// GBM3D_NO_SMALL_DIRECT=1 turns the rule off (the parity tests keep the tile kernels on their
+// small edge-case images).
+constexpr double kSmallDirectWork = 1.2e8;
+static bool small_direct(const MatchParams& p) {
+    static const bool off = getenv("GBM3D_NO_SMALL_DIRECT") != nullptr;
+    if (off) return false;
+    const double side = 2.0 * p.r + 1.0;
+    const double work = (double)p.B * (double)(p.row_end - p.row_begin) * (double)p.Rx * side * side *
+                        (double)p.P * (double)p.P;
+    return work < kSmallDirectWork;
+}
+
 static int run(const MatchParams& p, int method, cudaStream_t st) {
     int launches = 0;
     cudaError_t e = cudaSuccess;
     bool fast = false;
+    if (method == GBM3D_METHOD_AUTO && small_direct(p)) method = GBM3D_METHOD_DIRECT;
     const int kr1_ = std::min(p.row_end, p.Ry_reg);
     const bool app_col = p.Rx > p.Rx_reg && kr1_ > p.row_begin;
     const bool app_row = p.Ry > p.Ry_reg && p.row_end > p.Ry_reg;

@@ -4,6 +4,10 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# AUTO sends tiny jobs to the per-reference direct kernel (gbm3d_api.cu, small_direct); the
+# parity tests' small edge-case images must keep exercising the tile kernels they were written
+# for, so the rule is off here and tested on its own (test_auto_small_jobs_direct, subprocess).
+os.environ.setdefault("GBM3D_NO_SMALL_DIRECT", "1")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

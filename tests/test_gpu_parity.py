@@ -508,3 +508,35 @@ def test_fuzz_p12_and_direct_p16():
             i, d, n = g.block_match(torch.from_numpy(imgs).cuda(), P, s, r, K, tau)
             _assert_same((i.cpu().numpy(), d.cpu().numpy(), n.cpu().numpy()),
                          oracle.block_match_batched(imgs, P, s, r, K, tau), what + " batched")
+
+
+def test_auto_small_jobs_direct():
+    """AUTO's latency rule: jobs below the pixel-work threshold (c0) run on the per-reference
+    direct kernel alone (one launch), larger ones (c1) on the tile kernels; both give the
+    oracle's tables.  Subprocess without GBM3D_NO_SMALL_DIRECT (set for the rest of the suite)."""
+    import json, os, subprocess, sys
+    code = r'''
+import json, sys, torch
+import paper_2103_10765_b200 as g
+from synth import CONFIGS, config_images
+out = {}
+for name in ("c0", "c1"):
+    c = CONFIGS[name].calls[0]
+    img = torch.from_numpy(config_images(name)[0]).cuda()
+    i, d, n = g.block_match(img, c.patch, c.stride, c.radius, c.K, c.tau)
+    torch.cuda.synchronize()
+    out[name] = [g.last_launch_count(), i.cpu().numpy().tolist(), d.cpu().numpy().tolist(),
+                 n.cpu().numpy().tolist()]
+json.dump(out, sys.stdout)
+'''
+    env = {k: v for k, v in os.environ.items() if k != "GBM3D_NO_SMALL_DIRECT"}
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout)
+    assert got["c0"][0] == 1          # the direct kernel alone
+    assert got["c1"][0] > 1           # tile kernel (+ the appended row / column)
+    for name in ("c0", "c1"):
+        exp = _oracle_config(name, 0)
+        _assert_same(tuple(np.array(x, dtype=np.int32) for x in got[name][1:]), exp,
+                     f"AUTO small-job rule {name}")
