@@ -53,19 +53,26 @@ extern template cudaError_t launch_tc<3, 15>(const MatchParams&, cudaStream_t, i
 extern template cudaError_t launch_tc<3, 31>(const MatchParams&, cudaStream_t, int*, int);
 extern template cudaError_t launch_tc16<3, 15>(const MatchParams&, cudaStream_t, int*);
 extern template cudaError_t launch_tc16<3, 31>(const MatchParams&, cudaStream_t, int*);
-extern template cudaError_t launch_tcp<12, 4, 15>(const MatchParams&, cudaStream_t, int*);
-extern template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 15, 64>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 31, 64>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 15, 80>(const MatchParams&, cudaStream_t, int*);
+extern template cudaError_t launch_tcp<12, 4, 31, 80>(const MatchParams&, cudaStream_t, int*);
 static cudaError_t tc_dispatch(const MatchParams& p, cudaStream_t st, int* launches, bool* ok,
                                bool int8_only) {
     *ok = false;
     // patch 12 / stride 4 (c2): fp16 product form with in-kernel exact paths (tiles above the
     // fp16 bound; references whose 32-bit-key lists end short when tau - 1 > dsat); the tile's
-    // columns 7S + 2r + 1 <= 80 within the shared-memory bound (radius <= 21)
-    if (p.P == 12 && p.S == 4 && !int8_only && p.r <= tcp::MAX_R && 7 * p.S + 2 * p.r + 1 <= tcp::NB &&
+    // columns within N: 16 x 7 tiles when 6S + 2r + 1 <= 64, else 16 x 8 tiles with
+    // 7S + 2r + 1 <= 80 (radius <= 21, the shared-memory bound)
+    if (p.P == 12 && p.S == 4 && !int8_only && p.r <= tcp::MAX_R && 7 * p.S + 2 * p.r + 1 <= 80 &&
         p.K >= 2 && p.K <= 32) {
         *ok = true;
-        if (p.K - 1 <= 15) return launch_tcp<12, 4, 15>(p, st, launches);
-        return launch_tcp<12, 4, 31>(p, st, launches);
+        if (6 * p.S + 2 * p.r + 1 <= 64) {
+            if (p.K - 1 <= 15) return launch_tcp<12, 4, 15, 64>(p, st, launches);
+            return launch_tcp<12, 4, 31, 64>(p, st, launches);
+        }
+        if (p.K - 1 <= 15) return launch_tcp<12, 4, 15, 80>(p, st, launches);
+        return launch_tcp<12, 4, 31, 80>(p, st, launches);
     }
     if (p.P != 8 || p.S != 3 || 7 * p.S + 2 * p.r + 1 > tcm::NB || p.K < 2 || p.K > 32)
         return cudaSuccess;

@@ -11,11 +11,12 @@
 // Eq. (1) sums from the pixel plane), so every tile is bit-exact.
 //
 // Layout.
-//   * Tile = 16 x 8 grid references = MMA M = 128 (TMEM lane m = reference 8a + b); one CTA per
-//     tile (c2's 512^2 image: 124 tiles for 148 SMs, a single wave).
-//   * The union of the tile's windows is NT = 15S + 2r + 1 candidate rows x NJ = 7S + 2r + 1
-//     (<= NB = 80) candidate columns.  One candidate row = one M128 N80 product over K = 12 patch
-//     rows x 16 (the last 4 fp16 of every patch row are zero in A): 12 MMAs of K16.
+//   * Tile = 16 x TX grid references in MMA M = 128 (TMEM lane m = reference 8a + b, b < TX); one
+//     CTA per tile (c2's 512^2 image: 144 tiles of 16 x 7 for 148 SMs, a single wave).
+//   * The union of the tile's windows is NT = 15S + 2r + 1 candidate rows x NJ = (TX-1)S + 2r + 1
+//     candidate columns <= N (TX = 7, N = 64 when that fits, else TX = 8, N = 80).  One
+//     candidate row = one M128 xN product over K = 12 patch rows x 16 (the last 4 fp16 of every
+//     patch row are zero in A): 12 MMAs of K16.
 //   * B needs no per-row building: the tile's centred fp16 plane is written once pre-shifted,
 //     X[y][q][m][e] = plane[y][8q + m + e], so candidate row t's K16 step i (patch row i) is the
 //     canonical K-major operand at X + (t + i) * XP with LBO = SBO = 128 B (next 8 pixels of the
@@ -44,14 +45,24 @@
 
 namespace gbm3d {
 namespace tcp {
-constexpr int TY = 16, TX = 8;       // reference tile (grid rows x grid cols) = 128 MMA rows
-constexpr int NB = 80;               // candidate columns per MMA (N), >= 7S + 2r + 1
-constexpr int PW = 96;               // pixel plane pitch (int16): NB + 16
-constexpr int XQ = NB / 8;           // 16-byte pixel groups per pre-shifted row
-constexpr int XP = XQ * 128;         // bytes per pre-shifted plane row (8 shifts per group)
-constexpr int NTS = 5;               // accumulator stages in flight
-constexpr int SPITCH = NB;           // TMEM columns per stage
-constexpr int TM_A = (NTS * SPITCH + 31) / 32 * 32;  // A: 12 K16 steps x 8 columns (two fp16 each)
+constexpr int TY = 16;               // reference tile rows (grid rows); 8 lanes per grid row
+// Two tile shapes (template NBT): 16 x 7 references with N = 64 candidate columns when
+// 6S + 2r + 1 <= 64 (c2: r = 19), else 16 x 8 with N = 80 (r <= 21).  The narrower tile scans
+// a fifth fewer columns per row, holds six accumulator stages and a smaller plane, and c2's
+// 144 tiles still fit one wave on 148 SMs.  Lanes with b >= TX are idle.
+template <int NBT>
+struct Shape {
+    static constexpr int NB = NBT;                // candidate columns per MMA (N)
+    static constexpr int TX = NBT == 64 ? 7 : 8;  // reference tile columns (grid cols)
+    static constexpr int PW = NB + 16;            // pixel plane pitch (int16)
+    // 16-byte pixel groups per pre-shifted row: 10 for both shapes -- the last candidate
+    // group's second chunk (q + 1) and the exact path's reads (columns <= 77) stay in the row
+    static constexpr int XQ = 10;
+    static constexpr int XP = XQ * 128;           // bytes per pre-shifted row (8 shifts per group)
+    static constexpr int NTS = NBT == 64 ? 6 : 5;  // accumulator stages in flight
+    static constexpr int SPITCH = NB;             // TMEM columns per stage
+    static constexpr int TM_A = (NTS * SPITCH + 31) / 32 * 32;  // A: 12 K16 steps x 8 columns
+};
 #ifndef GBM3D_TCP_NH
 #define GBM3D_TCP_NH 1
 #endif
@@ -73,11 +84,14 @@ constexpr int MAX_R = 21;            // shared memory bound (see TcpGeom)
 struct TcpGeom {
     int NT, NJ, PR;
     int off_x, off_nq, off_raw, off_bar, total;
+    template <int NBT>
     __host__ __device__ static TcpGeom make(int P, int S, int r) {
         using namespace tcp;
+        using SH = Shape<NBT>;
+        constexpr int NB = SH::NB, PW = SH::PW, XP = SH::XP, NTS = SH::NTS;
         TcpGeom g;
         g.NT = 15 * S + 2 * r + 1;
-        g.NJ = 7 * S + 2 * r + 1;
+        g.NJ = (SH::TX - 1) * S + 2 * r + 1;
         g.PR = g.NT + P - 1;
         g.off_x = 0;                                          // X (+ one pad row); prologue: hs
         g.off_nq = (g.PR + 1) * XP;                           // candidate norms [NT][NB] fp32
@@ -155,13 +169,16 @@ static __device__ __forceinline__ uint32_t win_bits(int lo, int hi, int k) {
 }
 }  // namespace tcp
 
-template <int P, int S, int KL>
+template <int P, int S, int KL, int NBT>
 __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams p, int mmax) {
     using namespace tcp;
+    using SH = Shape<NBT>;
+    constexpr int NB = SH::NB, TX = SH::TX, PW = SH::PW, XQ = SH::XQ, XP = SH::XP;
+    constexpr int NTS = SH::NTS, SPITCH = SH::SPITCH, TM_A = SH::TM_A;
     static_assert(S % 4 == 0, "window staging in groups of 4 columns needs bS = S b aligned to 4");
     static_assert(TM_A + 8 * P <= (int)TMEM_COLS, "TMEM: accumulator stages + A");
     extern __shared__ __align__(1024) unsigned char sm[];
-    const TcpGeom g = TcpGeom::make(P, S, p.r);
+    const TcpGeom g = TcpGeom::make<NBT>(P, S, p.r);
     const int r = p.r, cb = p.cb;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kr1 = min(p.row_end, p.Ry_reg);
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(tcp::THREADS, 1) match_tcp_kernel(MatchParams 
         const int wq = warp & 3, h = warp >> 2;
         const int m = 32 * wq + lane, a = m >> 3, b = m & 7;
         const int ky = gy0 + a, kx = gx0 + b;
-        const bool active = ky < kr1 && kx < p.Rx_reg;
+        const bool active = b < TX && ky < kr1 && kx < p.Rx_reg;
         const int ry = ky * S, rx = kx * S;  // regular grid positions
         const int nfill = KL - (p.K - 1);    // sentinel zeros below the real keys
         uint32_t L[KL];
@@ -670,18 +687,19 @@ static inline int tcp_default_mmax(int P) {
     return M;
 }
 
-template <int P, int S, int KL>
+template <int P, int S, int KL, int NBT>
 cudaError_t launch_tcp(const MatchParams& p, cudaStream_t stream, int* launches) {
     const int kr0 = p.row_begin, kr1 = p.row_end < p.Ry_reg ? p.row_end : p.Ry_reg;
     if (kr1 <= kr0 || p.Rx_reg <= 0) return cudaSuccess;
-    const TcpGeom g = TcpGeom::make(P, S, p.r);
-    auto kern = match_tcp_kernel<P, S, KL>;
+    const TcpGeom g = TcpGeom::make<NBT>(P, S, p.r);
+    constexpr int TX = tcp::Shape<NBT>::TX;
+    auto kern = match_tcp_kernel<P, S, KL, NBT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.total);
     if (e != cudaSuccess) return e;
     // dev / test switch: a lower bound forces tiles onto the exact int32 path
     static const int mmax_env = getenv("GBM3D_TCP_MMAX") ? atoi(getenv("GBM3D_TCP_MMAX")) : -1;
     const int mmax = mmax_env >= 0 ? mmax_env : tcp_default_mmax(P);
-    dim3 grid((p.Rx_reg + tcp::TX - 1) / tcp::TX, (kr1 - kr0 + tcp::TY - 1) / tcp::TY, p.B);
+    dim3 grid((p.Rx_reg + TX - 1) / TX, (kr1 - kr0 + tcp::TY - 1) / tcp::TY, p.B);
     kern<<<grid, tcp::THREADS, g.total, stream>>>(p, mmax);
     if (launches) ++*launches;
     e = cudaGetLastError();
@@ -689,8 +707,8 @@ cudaError_t launch_tcp(const MatchParams& p, cudaStream_t stream, int* launches)
     static const bool dbg = getenv("GBM3D_DEBUG") != nullptr;
     if (dbg) {
         e = cudaStreamSynchronize(stream);
-        fprintf(stderr, "gbm3d: tcp P%d S%d grid %u x %u x %u smem %d: %s\n", P, S, grid.x, grid.y,
-                grid.z, g.total, cudaGetErrorString(e));
+        fprintf(stderr, "gbm3d: tcp P%d S%d N%d grid %u x %u x %u smem %d: %s\n", P, S, NBT, grid.x,
+                grid.y, grid.z, g.total, cudaGetErrorString(e));
     }
     return e;
 }

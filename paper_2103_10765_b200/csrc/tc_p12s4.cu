@@ -1,8 +1,10 @@
 // Tensor-core product-form instantiations for patch 12, stride 4 (BASELINE c2): K-1 <= 15 / <= 31.
 #include "match_tcp.cuh"
 namespace gbm3d {
-template cudaError_t launch_tcp<12, 4, 15>(const MatchParams&, cudaStream_t, int*);
-template cudaError_t launch_tcp<12, 4, 31>(const MatchParams&, cudaStream_t, int*);
+template cudaError_t launch_tcp<12, 4, 15, 64>(const MatchParams&, cudaStream_t, int*);
+template cudaError_t launch_tcp<12, 4, 31, 64>(const MatchParams&, cudaStream_t, int*);
+template cudaError_t launch_tcp<12, 4, 15, 80>(const MatchParams&, cudaStream_t, int*);
+template cudaError_t launch_tcp<12, 4, 31, 80>(const MatchParams&, cudaStream_t, int*);
 }  // namespace gbm3d
 
 #if GBM3D_TCP_TRACE
